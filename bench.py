@@ -1,0 +1,343 @@
+#!/usr/bin/env python3
+"""bench.py — throughput of the paper's hot path on B200 (arXiv 1310.3809).
+
+Default (N = 1): config C2 of BASELINE.json — 2^24 independent (a, b, N) triples of 192-bit
+(L = 6) operands, K = 256 chained lazy Montgomery products per triple; one step = one
+ecm_mulmod_batch over the whole batch (inputs resident in HBM, 1.15 GiB > L2).  Metric:
+192-bit modmul/s.  The same JSON line carries ECM stage-1 curves/s on config C3 (B1 = 50000,
+2^20 curves, 190-bit N) measured in the same run (`ecm`), the roofline of the dominant
+kernel, the CPU oracle baseline, clocks sampled during the timed region, and the end-to-end
+number through the public API with host buffers.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--no-ecm]
+Multi-GPU: torchrun --nproc-per-node N bench.py --gpus N ...; mulmod shards are independent
+replicas (weak scaling, no collective); ECM shards the 2^20 curves by contiguous ranges and
+all-gathers the per-curve status bytes over NCCL (strong scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+L = 6
+C2_COUNT = 1 << 24
+C2_ITERS = 256
+FPE_MUL = 2 * L * L                      # 32x32->64 partial products per L-limb product
+FPE_LADDER_STEP = 18 * L * L + 2 * L     # 6M + 4S (sqr = (3L^2+L)/2)
+MULMODS_PER_STEP = 10
+SMS = 148
+WIDE_PER_CLK_SM = 32                     # measured: profiles/r01_imad_rates.jsonl
+
+
+def peaks():
+    p = {}
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    mhz = float(p.get("sm_max_mhz", 1965.0))
+    return {"sm_max_mhz": mhz, "fpe_peak": SMS * WIDE_PER_CLK_SM * mhz * 1e6, "hbm_gbs": float(p.get("hbm_gbs", 6650.0)),
+            "source": "MEASURED_PEAKS.json sm_max_mhz x 148 SMs x 32 IMAD.WIDE/clk/SM (measured)" if p else "fallback"}
+
+
+# ---------------------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in self.rows for j in range(4) if r[3 + j].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------------------
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def max_over_ranks(torch, x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(torch, ws):
+    torch.cuda.synchronize()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def time_steps(torch, fn, steps, ws):
+    """Times `steps` calls of fn with CUDA events on the current stream; returns (total_ms, per-step ms)."""
+    stream = torch.cuda.current_stream()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    barrier(torch, ws)
+    evs[0].record(stream)
+    for i in range(steps):
+        fn()
+        evs[i + 1].record(stream)
+    torch.cuda.synchronize()
+    per = [evs[i].elapsed_time(evs[i + 1]) for i in range(steps)]
+    total = evs[0].elapsed_time(evs[-1])
+    barrier(torch, ws)
+    return total, per
+
+
+def ncu_traffic(name):
+    """dram bytes per launch for a kernel from the committed ncu summary (profiles/)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return d.get(name)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------------------
+def cpu_baseline_mulmod(sample_elems: int, iters: int):
+    import oracle
+    from workload import mulmod_inputs
+    a, b, n = mulmod_inputs(sample_elems, L, seed=2)
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    oracle.mulmod_chain_mt(a, b, n, L, iters, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": sample_elems * iters / dt, "unit": "modmul/s", "cores": threads, "kind": "oracle",
+            "sample": f"first {sample_elems} of C2's 2^24 triples x K={iters} (oracle C, {threads} host threads)",
+            "seconds": dt}
+
+
+def cpu_baseline_ecm(N, k, sigmas, B1):
+    import oracle
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    oracle.ecm_stage1_mt(N, L, k, sigmas, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": len(sigmas) / dt, "unit": "curves/s", "cores": threads, "kind": "oracle",
+            "sample": f"{len(sigmas)} of C3's curves at B1={B1}", "seconds": dt}
+
+
+# ---------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    import paper_1310_3809_b200 as eg
+    from paper_1310_3809_b200 import build as _b
+    _b.build()
+    from workload import ecm_config, mulmod_inputs
+
+    pk = peaks()
+    # ---------------- C2: batched 192-bit mulmod, K = 256, this rank's replica shard ----------------
+    count = args.count
+    a, b, n = mulmod_inputs(count, L, seed=2, start=rank * count)
+    A, B, Nn = (torch.from_numpy(x).cuda() for x in (a, b, n))
+    out = torch.empty_like(A)
+    step = lambda: eg.ecm_mulmod_batch(A, B, Nn, out, L=L, iters=args.iters)  # noqa: E731
+    for _ in range(args.warmup):
+        step()
+    with ClockSampler(local) as clk:
+        total_ms, per = time_steps(torch, step, args.steps, ws)
+    total_ms = max_over_ranks(torch, total_ms, ws)
+    mulmods = count * args.iters * args.steps * ws
+    value = mulmods / (total_ms * 1e-3)
+    kernel_ms = sum(per) / len(per)
+    fpe_launch = count * args.iters * FPE_MUL
+    achieved = fpe_launch / (kernel_ms * 1e-3)
+    clocks = clk.summary()
+
+    # ---------------- end to end: public API with host (pinned) buffers ----------------
+    ah, bh, nh = (torch.from_numpy(x).pin_memory() for x in (a, b, n))
+    oh = torch.empty_like(ah).pin_memory()
+    e2e_step = lambda: eg.ecm_mulmod_batch(ah, bh, nh, oh, L=L, iters=args.iters,  # noqa: E731
+                                           flags=eg.ECM_HOST_BUFFERS)
+    e2e_step()
+    barrier(torch, ws)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    barrier(torch, ws)
+    e2e_s = max_over_ranks(torch, time.perf_counter() - t0, ws)
+    e2e = {"value": mulmods / e2e_s, "unit": "modmul/s", "h2d_bytes_per_step": int(3 * a.nbytes),
+           "d2h_bytes_per_step": int(a.nbytes)}
+    del ah, bh, nh, oh
+
+    # ---------------- C3: ECM stage 1 curves/s (strong scaling over ranks) ----------------
+    ecm = None
+    if not args.no_ecm:
+        cfg = ecm_config("C3")
+        curves = cfg["curves"] if args.ecm_curves is None else args.ecm_curves
+        lo, hi = rank * curves // ws, (rank + 1) * curves // ws
+        sig = torch.from_numpy(cfg["sigmas"][lo:hi].copy()).cuda()
+        kb = eg.ecm_stage1_kbits(cfg["B1"])
+        eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], sig[:4096], want=("g",))  # warm-up (plan, code)
+        gathered = None
+
+        def ecm_step():
+            nonlocal gathered
+            r = eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], sig, want=("g",))
+            if ws > 1:
+                import torch.distributed as dist
+                gathered = torch.empty(curves, dtype=torch.uint8, device="cuda")
+                dist.all_gather_into_tensor(gathered, r["status"])
+            else:
+                gathered = r["status"]
+            return r
+
+        with ClockSampler(local) as clk2:
+            ecm_ms, _ = time_steps(torch, ecm_step, 1, ws)
+        ecm_ms = max_over_ranks(torch, ecm_ms, ws)
+        st = gathered.cpu().numpy()
+        curves_s = curves / (ecm_ms * 1e-3)
+        fpe_curve = (kb - 1) * FPE_LADDER_STEP
+        ecm = {"workload": f"C3: ECM stage 1, B1={cfg['B1']}, {curves} curves, 190-bit N=p*q (planted 64-bit p)",
+               "curves_per_s": curves_s, "modmul_per_s": curves_s * (kb - 1) * MULMODS_PER_STEP,
+               "ms": ecm_ms, "k_bits": kb, "flagged_factor": int((st == 1).sum()), "scaling": "strong",
+               "roofline": {"bound": "alu", "achieved": curves_s / ws * fpe_curve / 1e12,
+                            "peak": pk["fpe_peak"] / 1e12, "unit": "Tpp/s",
+                            "frac": curves_s / ws * fpe_curve / pk["fpe_peak"]},
+               "clocks": clk2.summary()}
+
+    line = {
+        "metric": "192-bit Montgomery modmul/s",
+        "value": value, "unit": "modmul/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": f"C2: {count} independent (a,b,N) triples per GPU, L=6 (190-bit N), "
+                               f"K={args.iters} chained lazy Montgomery products", "L": L, "count_per_gpu": count,
+                   "iters": args.iters, "redc": "word-CIOS (default)", "l2": "inputs 1.15 GiB > L2 (no flush needed)",
+                   "parallelism": f"replicas x{ws}"},
+        "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": pk["fpe_peak"] / 1e12, "unit": "Tpp/s",
+                     "frac": achieved / pk["fpe_peak"], "traffic": ncu_traffic("mulmod_batch_kernel<6,0,false>"),
+                     "kernel": "ecm::mulmod_batch_kernel<6,0,false>", "kernel_ms": kernel_ms,
+                     "peak_source": pk["source"],
+                     "frac_at_measured_clock": (achieved / (SMS * WIDE_PER_CLK_SM * clocks["sm_mhz"] * 1e6))
+                     if clocks.get("sm_mhz") else None},
+        "clocks": clocks, "e2e": e2e, "gpu_launches": args.steps,
+    }
+    if ecm:
+        line["ecm"] = ecm
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline_mulmod(args.cpu_elems, args.iters)
+        if ecm:
+            cfg = ecm_config("C3")
+            import oracle
+            k, _ = oracle.stage1_k(cfg["B1"])
+            idx = np.arange(0, cfg["curves"], cfg["curves"] // args.cpu_curves)[: args.cpu_curves]
+            ecm["cpu_baseline"] = cpu_baseline_ecm(cfg["N"], k, cfg["sigmas"][idx], cfg["B1"])
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """The reference arm for this tier is the CPU oracle as it stands."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    sample = args.cpu_elems
+    for _ in range(args.warmup):
+        cpu_baseline_mulmod(max(1024, sample // 16), args.iters)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(cpu_baseline_mulmod(sample, args.iters))
+    dt = time.perf_counter() - t0
+    value = sample * args.iters * args.steps / dt
+    cb = dict(vals[-1])
+    cb["value"] = value
+    line = {"impl": "reference", "metric": "192-bit Montgomery modmul/s", "value": value, "unit": "modmul/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": f"C2 sample: {sample} of the 2^24 triples per step, L=6, K={args.iters}",
+                       "L": L, "iters": args.iters},
+            "cpu_baseline": cb, "e2e": {"value": value, "unit": "modmul/s", "h2d_bytes_per_step": 0,
+                                        "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--count", type=int, default=C2_COUNT)
+    ap.add_argument("--iters", type=int, default=C2_ITERS)
+    ap.add_argument("--no-ecm", action="store_true")
+    ap.add_argument("--ecm-curves", type=int, default=None)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-elems", type=int, default=1 << 17)
+    ap.add_argument("--cpu-curves", type=int, default=64)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -195,3 +195,35 @@ def ladder_trace(N: int, L: int, k: int, sigma: int):
         return st, None
     out = [[from_limbs(tr[s, j]) for j in range(4)] for s in range(kb)]
     return 0, out
+
+
+# ---------------------------------------------------------------------------------------
+# host-thread fan-out (marshalling only: chunks of independent elements / curves)
+# ---------------------------------------------------------------------------------------
+def _pool_map(fn, chunks, threads):
+    import concurrent.futures as cf
+    if threads <= 1 or len(chunks) <= 1:
+        return [fn(c) for c in chunks]
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:  # ctypes releases the GIL
+        return list(ex.map(fn, chunks))
+
+
+def mulmod_chain_mt(a, b, n, L, iters, square=False, canonical=False, threads=None):
+    a, b, n = (np.ascontiguousarray(x, dtype=np.uint32).reshape(-1, L) for x in (a, b, n))
+    threads = threads or os.cpu_count() or 1
+    count = a.shape[0]
+    step = max(1, -(-count // (threads * 4)))
+    idx = [(s, min(count, s + step)) for s in range(0, count, step)]
+    parts = _pool_map(lambda r: mulmod_chain(a[r[0]:r[1]], b[r[0]:r[1]], n[r[0]:r[1]], L, iters, square, canonical),
+                      idx, threads)
+    return np.concatenate(parts, axis=0)
+
+
+def ecm_stage1_mt(N, L, k, sigmas, threads=None):
+    sig = np.asarray(sigmas, dtype=np.uint64)
+    threads = threads or os.cpu_count() or 1
+    count = sig.size
+    step = max(1, -(-count // (threads * 2)))
+    idx = [(s, min(count, s + step)) for s in range(0, count, step)]
+    parts = _pool_map(lambda r: ecm_stage1(N, L, k, sig[r[0]:r[1]]), idx, threads)
+    return {key: np.concatenate([p[key] for p in parts], axis=0) for key in parts[0]}

@@ -1,0 +1,301 @@
+// mont.cuh — sm_100a multi-precision Montgomery arithmetic (device side of libecmgpu).
+//
+// Implements, per lane, the paper's modular arithmetic (arXiv 1310.3809 §2):
+//   * REDC in word-serial CIOS form, LAZY: no final subtraction, values stay
+//     in [0, 2N) by the Lemma because R = 2^(32L) >= 4N (reading G2/G3).
+//   * the paper's Theorem applied per word (REDC_KNOWNLOW): the low word of
+//     m_i*N_0 is known to be -t_0 (mod 2^32), so it is not multiplied; carry = (t_0 != 0).
+//     And block forms (REDC_CLASSIC: q = T*N' mod R, T + q*N with 4 quadrant products;
+//     REDC_BLOCKTHM: the Theorem literally, m0*b0 recovered from the congruence, 3 quadrants).
+//   * branch-free Reduction after Addition / Subtraction with 2N.
+//
+// Hardware mapping (measured, profiles/r01_imad_rates.jsonl): on sm_100a a PTX pair
+//   mad.lo.cc  d0, a, b, c0;  madc.hi.cc d1, a, b, c1;
+// is fused by ptxas into ONE `IMAD.WIDE.U32 {d1,d0}, P, a, b, {c1,c0}` with carry-in/out
+// predicates; it issues at 32 lanes/clk/SM (same pipe time as IMAD.HI, twice IMAD.LO).
+// One IMAD.WIDE = one 32x32->64 partial product ("FPE").  The schedule below therefore keeps
+// every product as an adjacent lo/hi pair into an even-aligned 64-bit accumulator:
+//   even products a_i*b_j (j even) land on word pairs (j, j+1)      -> accumulator E[0..L)
+//   odd  products a_i*b_j (j odd)  land on word pairs (j, j+1)      -> accumulator O[0..L)
+// (O[k] has weight 2^(32(k+1))).  Within a row no two pairs overlap, so each accumulator is
+// ONE carry chain of L/2 IMAD.WIDE.  The division by 2^32 at the end of a CIOS row is pure
+// register renaming: the next row's odd chain reads E[2..L) as its addends (the "shift").
+// L must be even (L in {4, 6, 8, 12}).
+#pragma once
+#include <cstdint>
+
+namespace ecm {
+
+enum RedcVariant : int { REDC_WORD = 0, REDC_KNOWNLOW = 1, REDC_BLOCKTHM = 2, REDC_CLASSIC = 3 };
+
+// ------------------------------------------------------------------------------------------
+// PTX carry-chain primitives.  The carry flag (CC.CF) is implicit state that links
+// consecutive statements; every wrapper is `asm volatile` so the compiler keeps their order.
+// ------------------------------------------------------------------------------------------
+namespace ptx {
+__device__ __forceinline__ uint32_t mul_lo(uint32_t a, uint32_t b) { uint32_t d; asm volatile("mul.lo.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d; }
+__device__ __forceinline__ uint32_t mul_hi(uint32_t a, uint32_t b) { uint32_t d; asm volatile("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d; }
+__device__ __forceinline__ uint32_t mad_lo_cc(uint32_t a, uint32_t b, uint32_t c) { uint32_t d; asm volatile("mad.lo.cc.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c)); return d; }
+__device__ __forceinline__ uint32_t madc_lo_cc(uint32_t a, uint32_t b, uint32_t c) { uint32_t d; asm volatile("madc.lo.cc.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c)); return d; }
+__device__ __forceinline__ uint32_t mad_hi_cc(uint32_t a, uint32_t b, uint32_t c) { uint32_t d; asm volatile("mad.hi.cc.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c)); return d; }
+__device__ __forceinline__ uint32_t madc_hi_cc(uint32_t a, uint32_t b, uint32_t c) { uint32_t d; asm volatile("madc.hi.cc.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c)); return d; }
+__device__ __forceinline__ uint32_t madc_hi(uint32_t a, uint32_t b, uint32_t c) { uint32_t d; asm volatile("madc.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c)); return d; }
+__device__ __forceinline__ uint32_t madc_lo(uint32_t a, uint32_t b, uint32_t c) { uint32_t d; asm volatile("madc.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c)); return d; }
+__device__ __forceinline__ uint32_t add_cc(uint32_t a, uint32_t b) { uint32_t d; asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d; }
+__device__ __forceinline__ uint32_t addc_cc(uint32_t a, uint32_t b) { uint32_t d; asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d; }
+__device__ __forceinline__ uint32_t addc(uint32_t a, uint32_t b) { uint32_t d; asm volatile("addc.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d; }
+__device__ __forceinline__ uint32_t sub_cc(uint32_t a, uint32_t b) { uint32_t d; asm volatile("sub.cc.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d; }
+__device__ __forceinline__ uint32_t subc_cc(uint32_t a, uint32_t b) { uint32_t d; asm volatile("subc.cc.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d; }
+__device__ __forceinline__ uint32_t subc(uint32_t a, uint32_t b) { uint32_t d; asm volatile("subc.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d; }
+}  // namespace ptx
+
+// n0inv = -N0^{-1} mod 2^32 (the word-level m' of PAPER.md:94): Newton/Hensel lifting,
+// x <- x(2 - N0 x) doubles the correct low bits; x0 = (3 N0) ^ 2 is correct to 5 bits.
+__device__ __forceinline__ uint32_t neg_inv32(uint32_t n0) {
+  uint32_t x = (3u * n0) ^ 2u;
+  x *= 2u - n0 * x;
+  x *= 2u - n0 * x;
+  x *= 2u - n0 * x;
+  return 0u - x;
+}
+
+// ------------------------------------------------------------------------------------------
+// Chains.  acc += a * v[par], par = 0 (even j) or 1 (odd j), as L/2 fused IMAD.WIDE.U32.
+// `cin` selects madc (consume a pending carry) vs mad for the first pair; `cout_free`
+// promises the chain cannot carry out (so the last op does not write CC).
+// ------------------------------------------------------------------------------------------
+template <int L, int PAR, bool CIN, bool COUT>
+__device__ __forceinline__ void chain(uint32_t (&d)[L], const uint32_t (&c)[L], uint32_t a, const uint32_t (&v)[L]) {
+#pragma unroll
+  for (int j = 0; j < L; j += 2) {
+    const uint32_t b = v[j + PAR];
+    if (j == 0 && !CIN) d[j] = ptx::mad_lo_cc(a, b, c[j]);
+    else d[j] = ptx::madc_lo_cc(a, b, c[j]);
+    if (j + 2 == L && !COUT) d[j + 1] = ptx::madc_hi(a, b, c[j + 1]);
+    else d[j + 1] = ptx::madc_hi_cc(a, b, c[j + 1]);
+  }
+}
+
+// Known-low even reduction chain: E += m*N_even where the low word of m*N_0 is the known
+// value -E_0 (b*m = -a mod R).  E_0 + lo(m N_0) = 0 (mod 2^32) carries iff
+// E_0 != 0, produced here by E_0 + 0xffffffff.  IMAD.HI replaces the first IMAD.WIDE.
+template <int L>
+__device__ __forceinline__ void chain_even_knownlow(uint32_t (&E)[L], uint32_t m, const uint32_t (&n)[L]) {
+  (void)ptx::add_cc(E[0], 0xffffffffu);
+  E[1] = ptx::madc_hi_cc(m, n[0], E[1]);
+#pragma unroll
+  for (int j = 2; j < L; j += 2) {
+    E[j] = ptx::madc_lo_cc(m, n[j], E[j]);
+    E[j + 1] = ptx::madc_hi_cc(m, n[j], E[j + 1]);
+  }
+  E[0] = 0;
+}
+
+// ------------------------------------------------------------------------------------------
+// Lazy Montgomery multiplication, word-serial (CIOS) with even/odd accumulators.
+// r = (x*y + q*N)/R, q = x*y*(-N^{-1}) mod R — the unique raw REDC value (no final
+// subtraction).  Preconditions: N odd, N < R/4, x, y < 2N  =>  r < 2N (Lemma, reading G3).
+// Invariant (start of row i): running value t = E + O*2^32 + cc*2^32 with t < y + N, so
+// every partial sum is < (3/4) 2^(32(L+1)): the odd chain never carries out and the even
+// chain's carry fits in O[L-1].
+// ------------------------------------------------------------------------------------------
+template <int L, int V>
+__device__ __forceinline__ void mont_mul_cios(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L],
+                                              const uint32_t (&n)[L], uint32_t n0inv) {
+  static_assert(L % 2 == 0 && L >= 2, "L must be even");
+  uint32_t E[L], O[L], Z[L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) Z[j] = 0;
+  // row 0: products only (pairs are disjoint: no carries)
+  chain<L, 1, false, false>(O, Z, x[0], y);
+  chain<L, 0, false, false>(E, Z, x[0], y);
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    if (i > 0) {
+      // t += x_i * y.  O holds the shifted even accumulator; the pending carry of the
+      // shift add (weight 2^32) enters the odd chain's first pair.
+      chain<L, 1, true, false>(O, O, x[i], y);
+      chain<L, 0, false, true>(E, E, x[i], y);
+      O[L - 1] = ptx::addc(O[L - 1], 0);
+    }
+    // m_i = t_0 * (-N^{-1}) mod 2^32;  t += m_i * N
+    const uint32_t m = E[0] * n0inv;
+    chain<L, 1, false, false>(O, O, m, n);
+    if (V == REDC_KNOWNLOW) chain_even_knownlow<L>(E, m, n);
+    else chain<L, 0, false, true>(E, E, m, n);
+    O[L - 1] = ptx::addc(O[L - 1], 0);
+    // t /= 2^32: E[0] == 0.  New even accumulator = O (+ E[1] at weight 1, carry pending);
+    // new odd accumulator = E[2..L) (weights 2^32..), top two words zero.
+    uint32_t nE[L], nO[L];
+#pragma unroll
+    for (int k = 0; k < L; ++k) nE[k] = O[k];
+    nE[0] = ptx::add_cc(nE[0], E[1]);
+#pragma unroll
+    for (int k = 0; k < L; ++k) nO[k] = (k + 2 < L) ? E[k + 2] : 0u;
+    if (i + 1 < L) {
+#pragma unroll
+      for (int k = 0; k < L; ++k) { E[k] = nE[k]; O[k] = nO[k]; }
+    } else {
+      // merge: r = nE + nO*2^32 + carry
+      r[0] = nE[0];
+#pragma unroll
+      for (int k = 1; k < L - 1; ++k) r[k] = ptx::addc_cc(nE[k], nO[k - 1]);
+      r[L - 1] = ptx::addc(nE[L - 1], nO[L - 2]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Block (SOS) forms of REDC, for the paper's ablation (Table 5).
+// T = x*y (2L words); q = (T mod R) * N' mod R; r = (T + q*N)/R.
+//   CLASSIC : q*N as a full product (4 half-size quadrants).
+//   BLOCKTHM: the Theorem: with q = q1 h + q0, N = N1 h + N0, h = 2^(32 L/2), only
+//             q1 N1, q1 N0, q0 N1 are multiplied; q0 N0 = -(T + (q1 N0 + q0 N1) h) mod R.
+// Both return the same unique raw value as mont_mul_cios.
+// ------------------------------------------------------------------------------------------
+template <int A, int B>
+__device__ __forceinline__ void mul_full(uint32_t (&t)[A + B], const uint32_t* a, const uint32_t* b) {
+  // schoolbook, row by row, each row one carry chain (lo pairs then hi pairs)
+#pragma unroll
+  for (int k = 0; k < A + B; ++k) t[k] = 0;
+#pragma unroll
+  for (int i = 0; i < A; ++i) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      // (c, t[i+j]) = a_i b_j + t[i+j] + c
+      const uint32_t lo = ptx::mad_lo_cc(a[i], b[j], t[i + j]);
+      const uint32_t hi = ptx::madc_hi(a[i], b[j], 0u);
+      t[i + j] = ptx::add_cc(lo, c);
+      c = ptx::addc(hi, 0u);
+    }
+    t[i + B] = c;
+  }
+}
+
+template <int L>
+__device__ __forceinline__ void mul_low_half(uint32_t (&q)[L], const uint32_t* a, const uint32_t* b) {
+  // q = a*b mod 2^(32L)
+#pragma unroll
+  for (int k = 0; k < L; ++k) q[k] = 0;
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; i + j < L; ++j) {
+      if (i + j == L - 1) {
+        q[i + j] = q[i + j] + a[i] * b[j] + c;
+      } else {
+        const uint32_t lo = ptx::mad_lo_cc(a[i], b[j], q[i + j]);
+        const uint32_t hi = ptx::madc_hi(a[i], b[j], 0u);
+        q[i + j] = ptx::add_cc(lo, c);
+        c = ptx::addc(hi, 0u);
+      }
+    }
+  }
+}
+
+template <int L, int V>
+__device__ __forceinline__ void mont_mul_block(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L],
+                                               const uint32_t (&n)[L], const uint32_t (&nprime)[L]) {
+  constexpr int H = L / 2;
+  uint32_t T[2 * L], q[L];
+  mul_full<L, L>(T, x, y);
+  mul_low_half<L>(q, T, nprime);  // step 1
+  uint32_t QN[2 * L];
+  if (V == REDC_CLASSIC) {
+    mul_full<L, L>(QN, q, n);
+  } else {
+    // q N = q1 N1 h^2 + (q1 N0 + q0 N1) h + q0 N0,  h = 2^(32H)
+    uint32_t hh[2 * H], m10[2 * H], m01[2 * H];
+    mul_full<H, H>(hh, q + H, n + H);
+    mul_full<H, H>(m10, q + H, n);
+    mul_full<H, H>(m01, q, n + H);
+    // mid = q1 N0 + q0 N1  (2H words + carry)
+    uint32_t mid[2 * H + 1];
+    mid[0] = ptx::add_cc(m10[0], m01[0]);
+#pragma unroll
+    for (int k = 1; k < 2 * H; ++k) mid[k] = ptx::addc_cc(m10[k], m01[k]);
+    mid[2 * H] = ptx::addc(0u, 0u);
+    // q0 N0 = -(T + mid h) mod R  (the congruence of the Theorem)
+    uint32_t s[L], q0n0[L];
+    s[0] = T[0];
+#pragma unroll
+    for (int k = 1; k < H; ++k) s[k] = T[k];
+    s[H] = ptx::add_cc(T[H], mid[0]);
+#pragma unroll
+    for (int k = H + 1; k < L; ++k) s[k] = ptx::addc_cc(T[k], mid[k - H]);
+    q0n0[0] = ptx::sub_cc(0u, s[0]);
+#pragma unroll
+    for (int k = 1; k < L; ++k) q0n0[k] = ptx::subc_cc(0u, s[k]);
+    // QN = q0n0 + mid h + hh h^2
+#pragma unroll
+    for (int k = 0; k < 2 * L; ++k) QN[k] = (k < L) ? q0n0[k] : 0u;
+    QN[H] = ptx::add_cc(QN[H], mid[0]);
+#pragma unroll
+    for (int k = H + 1; k < 2 * L; ++k) QN[k] = ptx::addc_cc(QN[k], (k - H <= 2 * H) ? mid[k - H] : 0u);
+    QN[L] = ptx::add_cc(QN[L], hh[0]);
+#pragma unroll
+    for (int k = L + 1; k < 2 * L; ++k) QN[k] = ptx::addc_cc(QN[k], hh[k - L]);
+  }
+  // r = (T + QN) / R  (low half is zero by construction; only its carry matters)
+  uint32_t lo = ptx::add_cc(T[0], QN[0]);
+#pragma unroll
+  for (int k = 1; k < L; ++k) lo = ptx::addc_cc(T[k], QN[k]);
+  (void)lo;
+#pragma unroll
+  for (int k = 0; k < L - 1; ++k) r[k] = ptx::addc_cc(T[L + k], QN[L + k]);
+  r[L - 1] = ptx::addc(T[2 * L - 1], QN[2 * L - 1]);
+}
+
+// ------------------------------------------------------------------------------------------
+// Lazy add / sub in [0, 2N) with a precomputed 2N: both candidates
+// are formed and the carry/borrow bit selects — no data-dependent branch.
+// ------------------------------------------------------------------------------------------
+template <int L>
+__device__ __forceinline__ void add_lazy(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L], const uint32_t (&n2)[L]) {
+  uint32_t s[L], d[L];
+  s[0] = ptx::add_cc(x[0], y[0]);
+#pragma unroll
+  for (int k = 1; k < L; ++k) s[k] = ptx::addc_cc(x[k], y[k]);
+  // x + y < 4N < R: no carry out of s.  d = s - 2N; keep s if it borrowed.
+  d[0] = ptx::sub_cc(s[0], n2[0]);
+#pragma unroll
+  for (int k = 1; k < L; ++k) d[k] = ptx::subc_cc(s[k], n2[k]);
+  const uint32_t borrow = ptx::subc(0u, 0u);  // 0 or 0xffffffff
+#pragma unroll
+  for (int k = 0; k < L; ++k) r[k] = borrow ? s[k] : d[k];
+}
+
+template <int L>
+__device__ __forceinline__ void sub_lazy(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L], const uint32_t (&n2)[L]) {
+  uint32_t d[L];
+  d[0] = ptx::sub_cc(x[0], y[0]);
+#pragma unroll
+  for (int k = 1; k < L; ++k) d[k] = ptx::subc_cc(x[k], y[k]);
+  const uint32_t mask = ptx::subc(0u, 0u);  // all ones iff x < y (reading G4: add 2N then)
+  r[0] = ptx::add_cc(d[0], n2[0] & mask);
+#pragma unroll
+  for (int k = 1; k < L - 1; ++k) r[k] = ptx::addc_cc(d[k], n2[k] & mask);
+  r[L - 1] = ptx::addc(d[L - 1], n2[L - 1] & mask);
+}
+
+// r = x - N if x >= N else x  (canonical representative of a lazy value in [0, 2N))
+template <int L>
+__device__ __forceinline__ void canonicalize(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&n)[L]) {
+  uint32_t d[L];
+  d[0] = ptx::sub_cc(x[0], n[0]);
+#pragma unroll
+  for (int k = 1; k < L; ++k) d[k] = ptx::subc_cc(x[k], n[k]);
+  const uint32_t borrow = ptx::subc(0u, 0u);
+#pragma unroll
+  for (int k = 0; k < L; ++k) r[k] = borrow ? x[k] : d[k];
+}
+
+template <int L>
+__device__ __forceinline__ void mont_mul(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L],
+                                         const uint32_t (&n)[L], uint32_t n0inv) {
+  mont_mul_cios<L, REDC_WORD>(r, x, y, n, n0inv);
+}
+
+}  // namespace ecm

@@ -1,0 +1,248 @@
+// mulmod.cu — batched lazy Montgomery multiplication chains (ecm_mulmod_batch), sm_100a.
+//
+// One lane = one independent (a_i, b_i, n_i) triple (north_star: "one independent modulus and
+// operand set per lane").  Stage-in: a warp moves its 32-element tile (32*L contiguous words in
+// the AoS layout) with 128-bit loads into a warp-private shared-memory tile, then each lane
+// reads its own L words (64-bit LDS, bank-conflict free for L = 6, 12).  Hot loop: `iters`
+// dependent Montgomery products entirely in registers (mont.cuh).  Stage-out mirrors stage-in.
+// The limb-sliced layout (ECM_LAYOUT_SLICED) needs no staging: limb j of the warp's 32
+// elements is one coalesced 128-byte row.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+#include "mont.cuh"
+
+namespace ecm {
+
+constexpr int kMulmodTPB = 256;
+
+// -N^{-1} mod R over the full width, for the block (SOS) REDC variants: Newton lifting
+// x <- x (2 - N x) of N^{-1} from the 32-bit inverse, doubling the correct words.
+template <int L>
+__device__ __forceinline__ void nprime_full(uint32_t (&np)[L], const uint32_t (&n)[L]) {
+  uint32_t x[L];
+#pragma unroll
+  for (int k = 0; k < L; ++k) x[k] = 0;
+  x[0] = 0u - neg_inv32(n[0]);  // N^{-1} mod 2^32
+#pragma unroll
+  for (int correct = 1; correct < L; correct *= 2) {
+    uint32_t t[L], u[L];
+    mul_low_half<L>(t, n, x);  // t = N x
+    // u = 2 - t  (mod R)
+    u[0] = ptx::sub_cc(2u, t[0]);
+#pragma unroll
+    for (int k = 1; k < L; ++k) u[k] = ptx::subc_cc(0u, t[k]);
+    mul_low_half<L>(t, x, u);
+#pragma unroll
+    for (int k = 0; k < L; ++k) x[k] = t[k];
+  }
+  np[0] = ptx::sub_cc(0u, x[0]);
+#pragma unroll
+  for (int k = 1; k < L; ++k) np[k] = ptx::subc_cc(0u, x[k]);
+}
+
+// Warp-cooperative AoS tile load: words [e0*L, e0*L + nvalid*L) -> smem tile, then lane's L words.
+template <int L>
+__device__ __forceinline__ void load_aos(uint32_t (&v)[L], const uint32_t* __restrict__ g, uint32_t* tile,
+                                         size_t e0, int nvalid, int lane) {
+  const uint32_t* src = g + e0 * L;
+  if (nvalid == 32) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* t4 = reinterpret_cast<uint4*>(tile);
+#pragma unroll
+    for (int k = lane; k < 8 * L; k += 32) t4[k] = __ldcs(s4 + k);
+  } else {
+    for (int k = lane; k < nvalid * L; k += 32) tile[k] = __ldcs(src + k);
+  }
+  __syncwarp();
+  const uint2* t2 = reinterpret_cast<const uint2*>(tile) + lane * (L / 2);
+#pragma unroll
+  for (int k = 0; k < L / 2; ++k) {
+    const uint2 w = t2[k];
+    v[2 * k] = w.x;
+    v[2 * k + 1] = w.y;
+  }
+  __syncwarp();
+}
+
+template <int L>
+__device__ __forceinline__ void store_aos(uint32_t* __restrict__ g, const uint32_t (&v)[L], uint32_t* tile,
+                                          size_t e0, int nvalid, int lane) {
+  uint2* t2 = reinterpret_cast<uint2*>(tile) + lane * (L / 2);
+#pragma unroll
+  for (int k = 0; k < L / 2; ++k) t2[k] = make_uint2(v[2 * k], v[2 * k + 1]);
+  __syncwarp();
+  uint32_t* dst = g + e0 * L;
+  if (nvalid == 32) {
+    const uint4* t4 = reinterpret_cast<const uint4*>(tile);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int k = lane; k < 8 * L; k += 32) __stcs(d4 + k, t4[k]);
+  } else {
+    for (int k = lane; k < nvalid * L; k += 32) dst[k] = tile[k];
+  }
+  __syncwarp();
+}
+
+template <int L, int V, bool SQUARE>
+__global__ void __launch_bounds__(kMulmodTPB) mulmod_batch_kernel(const uint32_t* __restrict__ a,
+                                                                  const uint32_t* __restrict__ b,
+                                                                  const uint32_t* __restrict__ n,
+                                                                  uint32_t* out, size_t count, uint32_t iters,
+                                                                  uint32_t flags) {
+  __shared__ __align__(16) uint32_t smem[kMulmodTPB * L];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  uint32_t* tile = smem + warp * 32 * L;
+  const bool sliced = flags & 0x4u;
+  const bool canon = flags & 0x1u;
+  const size_t ntiles = (count + 31) / 32;
+  const size_t warps_total = (size_t)gridDim.x * (kMulmodTPB / 32);
+  for (size_t wt = (size_t)blockIdx.x * (kMulmodTPB / 32) + warp; wt < ntiles; wt += warps_total) {
+    const size_t e0 = wt * 32;
+    const int nvalid = (int)((count - e0) < 32 ? (count - e0) : 32);
+    const size_t e = e0 + lane;
+    uint32_t x[L], y[L], nn[L];
+    if (sliced) {
+      if (lane < nvalid) {
+#pragma unroll
+        for (int k = 0; k < L; ++k) {
+          x[k] = __ldcs(a + (size_t)k * count + e);
+          nn[k] = __ldcs(n + (size_t)k * count + e);
+          y[k] = SQUARE ? 0u : __ldcs(b + (size_t)k * count + e);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < L; ++k) x[k] = y[k] = nn[k] = 0;
+        nn[0] = 1;
+      }
+    } else {
+      load_aos<L>(x, a, tile, e0, nvalid, lane);
+      if (!SQUARE) load_aos<L>(y, b, tile, e0, nvalid, lane);
+      load_aos<L>(nn, n, tile, e0, nvalid, lane);
+      if (lane >= nvalid) nn[0] |= 1u;  // keep dead lanes' arithmetic well-defined
+    }
+    const uint32_t n0inv = neg_inv32(nn[0]);
+    uint32_t np[L];
+    if (V == REDC_BLOCKTHM || V == REDC_CLASSIC) nprime_full<L>(np, nn);
+    // ---- hot loop: iters dependent lazy Montgomery products, all in registers ----
+#pragma unroll 1
+    for (uint32_t t = 0; t < iters; ++t) {
+      uint32_t r[L];
+      if (V == REDC_WORD || V == REDC_KNOWNLOW) {
+        if (SQUARE) mont_mul_cios<L, V>(r, x, x, nn, n0inv);
+        else mont_mul_cios<L, V>(r, x, y, nn, n0inv);
+      } else {
+        if (SQUARE) mont_mul_block<L, V>(r, x, x, nn, np);
+        else mont_mul_block<L, V>(r, x, y, nn, np);
+      }
+#pragma unroll
+      for (int k = 0; k < L; ++k) x[k] = r[k];
+    }
+    if (canon) {
+      uint32_t r[L];
+      canonicalize<L>(r, x, nn);
+#pragma unroll
+      for (int k = 0; k < L; ++k) x[k] = r[k];
+    }
+    if (sliced) {
+      if (lane < nvalid) {
+#pragma unroll
+        for (int k = 0; k < L; ++k) __stcs(out + (size_t)k * count + e, x[k]);
+      }
+    } else {
+      store_aos<L>(out, x, tile, e0, nvalid, lane);
+    }
+  }
+}
+
+// ---- precondition check (ECM_CHECK): n odd, bitlen(n) <= 32L-2, a, b < 2n ----
+template <int L>
+__global__ void mulmod_check_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                                    const uint32_t* __restrict__ n, size_t count, uint32_t flags,
+                                    uint32_t* err) {
+  const bool sliced = flags & 0x4u, square = flags & 0x2u;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    uint32_t x[L], y[L], nn[L], n2[L + 1];
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+      const size_t off = sliced ? (size_t)k * count + i : i * L + k;
+      x[k] = a[off];
+      y[k] = square ? 0u : b[off];
+      nn[k] = n[off];
+    }
+    uint32_t code = 0;
+    if (!(nn[0] & 1u) || (L == 1 && nn[0] < 3)) code = 2;  // ECM_E_MODULUS
+    else if (nn[L - 1] >> 30) code = 3;                    // ECM_E_WIDTH
+    else {
+      // 2n (fits L words since n < 2^(32L-2))
+      uint32_t c = 0;
+#pragma unroll
+      for (int k = 0; k < L; ++k) {
+        n2[k] = (nn[k] << 1) | c;
+        c = nn[k] >> 31;
+      }
+      // x < 2n and y < 2n ?
+      bool xlt = false, ylt = false, xd = false, yd = false;
+#pragma unroll
+      for (int k = L - 1; k >= 0; --k) {
+        if (!xd && x[k] != n2[k]) { xlt = x[k] < n2[k]; xd = true; }
+        if (!yd && y[k] != n2[k]) { ylt = y[k] < n2[k]; yd = true; }
+      }
+      if (!xlt || !ylt) code = 5;  // ECM_E_RANGE
+    }
+    if (code) atomicMax(err, code);
+  }
+}
+
+template <int L, int V>
+static cudaError_t launch_mulmod_LV(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out,
+                                    size_t count, uint32_t iters, uint32_t flags, cudaStream_t s) {
+  const size_t ntiles = (count + 31) / 32;
+  size_t blocks = (ntiles + (kMulmodTPB / 32) - 1) / (kMulmodTPB / 32);
+  if (blocks > 0x7fffffffull) blocks = 0x7fffffffull;
+  if (flags & 0x2u)
+    mulmod_batch_kernel<L, V, true><<<(unsigned)blocks, kMulmodTPB, 0, s>>>(a, b, n, out, count, iters, flags);
+  else
+    mulmod_batch_kernel<L, V, false><<<(unsigned)blocks, kMulmodTPB, 0, s>>>(a, b, n, out, count, iters, flags);
+  return cudaGetLastError();
+}
+
+template <int L>
+static cudaError_t launch_mulmod_L(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out,
+                                   size_t count, uint32_t iters, uint32_t flags, cudaStream_t s) {
+  switch ((flags >> 8) & 3u) {
+    case REDC_WORD: return launch_mulmod_LV<L, REDC_WORD>(a, b, n, out, count, iters, flags, s);
+    case REDC_KNOWNLOW: return launch_mulmod_LV<L, REDC_KNOWNLOW>(a, b, n, out, count, iters, flags, s);
+    case REDC_BLOCKTHM: return launch_mulmod_LV<L, REDC_BLOCKTHM>(a, b, n, out, count, iters, flags, s);
+    default: return launch_mulmod_LV<L, REDC_CLASSIC>(a, b, n, out, count, iters, flags, s);
+  }
+}
+
+cudaError_t launch_mulmod(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out, size_t count,
+                          int L, uint32_t iters, uint32_t flags, cudaStream_t s) {
+  switch (L) {
+    case 4: return launch_mulmod_L<4>(a, b, n, out, count, iters, flags, s);
+    case 6: return launch_mulmod_L<6>(a, b, n, out, count, iters, flags, s);
+    case 8: return launch_mulmod_L<8>(a, b, n, out, count, iters, flags, s);
+    case 12: return launch_mulmod_L<12>(a, b, n, out, count, iters, flags, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_mulmod_check(const uint32_t* a, const uint32_t* b, const uint32_t* n, size_t count, int L,
+                                uint32_t flags, uint32_t* err, cudaStream_t s) {
+  const unsigned blocks = (unsigned)((count + 255) / 256 < 4096 ? (count + 255) / 256 : 4096);
+  switch (L) {
+    case 4: mulmod_check_kernel<4><<<blocks, 256, 0, s>>>(a, b, n, count, flags, err); break;
+    case 6: mulmod_check_kernel<6><<<blocks, 256, 0, s>>>(a, b, n, count, flags, err); break;
+    case 8: mulmod_check_kernel<8><<<blocks, 256, 0, s>>>(a, b, n, count, flags, err); break;
+    case 12: mulmod_check_kernel<12><<<blocks, 256, 0, s>>>(a, b, n, count, flags, err); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ecm

@@ -1,0 +1,135 @@
+"""GPU parity: ecm_stage1_batch / ecm_ladder_batch (through the C ABI) vs the CPU oracle.
+
+Bit-exact on every output (X, Z, g, status, xaff) for C1 (all 256 curves), for every width on
+small configs with ragged curve counts, for degenerate seeds; [#E(F_p)]P = O on small primes
+with brute-force group orders; C3 at full size (2^20 curves, B1 = 50000 — the launch bench.py
+times for ECM) on a strided sample plus every flagged g checked by division.
+"""
+import numpy as np
+import pytest
+
+import paper_1310_3809_b200 as eg
+from workload import ecm_config
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_1310_3809_b200 import build
+    build.build()
+    return torch
+
+
+def gpu_stage1(torch, N, L, B1, sig, **kw):
+    s = torch.from_numpy(np.ascontiguousarray(sig, dtype=np.uint64)).cuda()
+    r = eg.ecm_stage1_batch(N, L, B1, s, **kw)
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in r.items()}
+
+
+def assert_same(got, want, keys=("X", "Z", "g", "status", "xaff")):
+    for k in keys:
+        assert np.array_equal(got[k], want[k]), k
+
+
+def test_c1_all_curves_bit_exact(orc, torch):
+    cfg = ecm_config("C1")
+    k, _ = orc.stage1_k(cfg["B1"])
+    got = gpu_stage1(torch, cfg["N"], cfg["L"], cfg["B1"], cfg["sigmas"])
+    want = orc.ecm_stage1_mt(cfg["N"], cfg["L"], k, cfg["sigmas"])
+    assert_same(got, want)
+    found = got["status"] == 1
+    assert 10 <= found.sum() <= 45
+    for row in got["g"][found]:
+        assert eg.limbs_to_int(row) == cfg["p"]
+
+
+@pytest.mark.parametrize("L,nbits,pbits", [(4, 126, 30), (6, 190, 40), (8, 254, 40), (12, 382, 40)])
+def test_widths_ragged_counts(orc, torch, L, nbits, pbits):
+    cfg = ecm_config(L=L, nbits=nbits, pbits=pbits, B1=400, curves=77, seed=20 + L)
+    k, _ = orc.stage1_k(cfg["B1"])
+    got = gpu_stage1(torch, cfg["N"], L, cfg["B1"], cfg["sigmas"])
+    want = orc.ecm_stage1_mt(cfg["N"], L, k, cfg["sigmas"])
+    assert_same(got, want)
+
+
+def test_ladder_explicit_scalars(orc, torch):
+    cfg = ecm_config(L=6, nbits=190, pbits=32, B1=100, curves=40, seed=31)
+    s = torch.from_numpy(cfg["sigmas"]).cuda()
+    for k in (1, 2, 3, 4, 5, 7, 0x1F3, (1 << 200) + 12345, 2520):
+        r = eg.ecm_ladder_batch(cfg["N"], 6, k, s)
+        got = {kk: v.cpu().numpy() for kk, v in r.items()}
+        want = orc.ecm_stage1(cfg["N"], 6, k, cfg["sigmas"])
+        assert_same(got, want)
+
+
+def _curve_order(orc, p, sigma):
+    st, x0, a24, _ = orc.suyama(p, 1, sigma)
+    if st:
+        return None
+    A = (4 * a24 - 2) % p
+    B = (x0 ** 3 + A * x0 * x0 + x0) % p
+    if B == 0 or (A * A - 4) % p == 0:
+        return None
+    Binv = pow(B, -1, p)
+    n = 1
+    for x in range(p):
+        r = (x * x * x + A * x * x + x) * Binv % p
+        n += 1 if r == 0 else (2 if pow(r, (p - 1) // 2, p) == 1 else 0)
+    return n
+
+
+@pytest.mark.parametrize("p", [1009, 2003, 4093])
+def test_group_order_kills_point(orc, torch, p):
+    """[#E(F_p)]P = O: Z == 0, status ALL, g = p; with N = p in L = 4."""
+    for sigma in range(6, 14):
+        nE = _curve_order(orc, p, sigma)
+        if nE is None:
+            continue
+        s = torch.tensor([sigma], dtype=torch.uint64).cuda()
+        r = eg.ecm_ladder_batch(p, 4, nE, s)
+        assert int(r["status"][0]) == 2
+        assert eg.limbs_to_int(r["Z"][0].cpu().numpy()) == 0
+        assert eg.limbs_to_int(r["g"][0].cpu().numpy()) == p
+
+
+def test_degenerate_sigmas(orc, torch):
+    # 15^2 - 5 = 220 = 20*11: u = 0 mod 11.  N = 11*13 -> setup factor 11; N = 11 -> status 3
+    got = gpu_stage1(torch, 143, 4, 50, np.array([15, 6, 7], np.uint64))
+    k, _ = orc.stage1_k(50)
+    want = orc.ecm_stage1(143, 4, k, [15, 6, 7])
+    assert_same(got, want)
+    assert got["status"][0] == 4 and eg.limbs_to_int(got["g"][0]) == 11
+    got = gpu_stage1(torch, 11, 4, 50, np.array([15], np.uint64))
+    assert got["status"][0] == 3
+
+
+def test_host_buffers_and_no_xaff(orc, torch):
+    cfg = ecm_config(L=6, nbits=190, pbits=32, B1=300, curves=50, seed=41)
+    k, _ = orc.stage1_k(cfg["B1"])
+    r = eg.ecm_stage1_batch(cfg["N"], 6, cfg["B1"], cfg["sigmas"].copy(), flags=eg.ECM_HOST_BUFFERS)
+    want = orc.ecm_stage1(cfg["N"], 6, k, cfg["sigmas"])
+    assert_same(r, want)
+    got = gpu_stage1(torch, cfg["N"], 6, cfg["B1"], cfg["sigmas"], want=("X", "Z", "g"))
+    assert_same(got, want, keys=("X", "Z", "g", "status"))
+
+
+def test_c3_full_size_sampled(orc, torch):
+    """C3 (B1 = 50000, 2^20 curves, 190-bit N with a planted 64-bit p): 256 strided curves
+    bit-exact vs the oracle; every flagged g divides N."""
+    cfg = ecm_config("C3")
+    N, L = cfg["N"], cfg["L"]
+    got = gpu_stage1(torch, N, L, cfg["B1"], cfg["sigmas"], want=("X", "Z", "g"))
+    idx = np.arange(0, cfg["curves"], cfg["curves"] // 256) + 7
+    k, _ = orc.stage1_k(cfg["B1"])
+    want = orc.ecm_stage1_mt(N, L, k, cfg["sigmas"][idx])
+    sub = {key: v[idx] for key, v in got.items()}
+    assert_same(sub, want, keys=("X", "Z", "g", "status"))
+    flagged = np.nonzero(got["status"] == 1)[0]
+    assert len(flagged) > 1000  # Dickman estimate ~7k
+    for i in flagged[:: max(1, len(flagged) // 500)]:
+        g = eg.limbs_to_int(got["g"][i])
+        assert 1 < g < N and N % g == 0

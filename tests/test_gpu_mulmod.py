@@ -1,0 +1,159 @@
+"""GPU parity: ecm_mulmod_batch (through the C ABI) vs the CPU oracle, bit for bit.
+
+Small sizes span several warp tiles and a ragged tail for every width, mode, layout and REDC
+variant; C2 at full size (2^24 triples, the launch configuration bench.py times) is checked
+element by element for K = 1 and 16 and on a strided sample for K = 256, plus the Lemma bound
+out < 2N on every element.
+"""
+import numpy as np
+import pytest
+
+import paper_1310_3809_b200 as eg
+from workload import mulmod_inputs
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = {"word": eg.ECM_REDC_WORD, "knownlow": eg.ECM_REDC_KNOWNLOW,
+            "blockthm": eg.ECM_REDC_BLOCKTHM, "classic": eg.ECM_REDC_CLASSIC}
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_1310_3809_b200 import build
+    build.build()
+    return torch
+
+
+def dev(torch, x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def run_gpu(torch, a, b, n, L, iters, flags):
+    if flags & eg.ECM_LAYOUT_SLICED:
+        A, B, Nn = (dev(torch, x.T.copy()) for x in (a, b, n))
+        out = eg.ecm_mulmod_batch(A, B, Nn, L=L, iters=iters, flags=flags)
+        torch.cuda.synchronize()
+        return out.cpu().numpy().T.copy()
+    A, B, Nn = (dev(torch, x) for x in (a, b, n))
+    out = eg.ecm_mulmod_batch(A, B, Nn, L=L, iters=iters, flags=flags)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def lt_2n(x, n):
+    """Vectorised x < 2n for (count, L) limb arrays."""
+    L = n.shape[1]
+    n2 = np.zeros((n.shape[0], L + 1), np.uint64)
+    c = np.zeros(n.shape[0], np.uint64)
+    for j in range(L):
+        t = (n[:, j].astype(np.uint64) << np.uint64(1)) + c
+        n2[:, j] = t & np.uint64(0xFFFFFFFF)
+        c = t >> np.uint64(32)
+    n2[:, L] = c
+    less = np.zeros(n.shape[0], bool)
+    decided = np.zeros(n.shape[0], bool)
+    for j in range(L, -1, -1):
+        xj = x[:, j].astype(np.uint64) if j < L else np.zeros(n.shape[0], np.uint64)
+        lt, gt = xj < n2[:, j], xj > n2[:, j]
+        less |= ~decided & lt
+        decided |= lt | gt
+    return less
+
+
+@pytest.mark.parametrize("L", (4, 6, 8, 12))
+@pytest.mark.parametrize("square", (False, True))
+@pytest.mark.parametrize("layout", ("aos", "sliced"))
+def test_parity_small_all_widths(orc, torch, L, square, layout):
+    count = 32 * 37 + 5  # several tiles, ragged tail
+    a, b, n = mulmod_inputs(count, L, seed=100 + L, lazy=True)
+    flags = (eg.ECM_SQUARE if square else 0) | (eg.ECM_LAYOUT_SLICED if layout == "sliced" else 0)
+    for iters in (1, 16):
+        got = run_gpu(torch, a, b, n, L, iters, flags)
+        want = orc.mulmod_chain_mt(a, b, n, L, iters, square=square)
+        assert np.array_equal(got, want), (L, square, layout, iters)
+        assert lt_2n(got, n).all()
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
+@pytest.mark.parametrize("L", (4, 6, 8, 12))
+def test_parity_redc_variants_identical(orc, torch, variant, L):
+    """Every REDC variant returns the same unique raw value."""
+    count = 32 * 9 + 17
+    a, b, n = mulmod_inputs(count, L, seed=200 + L, lazy=True)
+    for square in (False, True):
+        flags = VARIANTS[variant] | (eg.ECM_SQUARE if square else 0)
+        got = run_gpu(torch, a, b, n, L, 7, flags)
+        want = orc.mulmod_chain_mt(a, b, n, L, 7, square=square)
+        assert np.array_equal(got, want), (variant, L, square)
+
+
+def test_canonical_flag_and_edges(orc, torch):
+    L = 6
+    a, b, n = mulmod_inputs(1000, L, seed=7, lazy=True)
+    # edge operands: 0, 1, 2n-1
+    a[0] = 0
+    b[1] = 0
+    a[2] = 0; a[2, 0] = 1
+    for i in (3, 4):  # 2n - 1
+        c = 0
+        for j in range(L):
+            t = (int(n[i, j]) << 1) + c
+            a[i, j] = t & 0xFFFFFFFF
+            c = t >> 32
+        a[i, 0] -= 1
+    b[4] = a[4]
+    for iters in (1, 3):
+        got = run_gpu(torch, a, b, n, L, iters, eg.ECM_CANONICAL)
+        want = orc.mulmod_chain_mt(a, b, n, L, iters, canonical=True)
+        assert np.array_equal(got, want)
+    assert not got[0].any() and not got[1].any()
+
+
+def test_single_element_and_check_flag(orc, torch):
+    L = 6
+    a, b, n = mulmod_inputs(1, L, seed=8)
+    got = run_gpu(torch, a, b, n, L, 5, 0)
+    assert np.array_equal(got, orc.mulmod_chain(a, b, n, L, 5))
+    A, B, Nn = (dev(torch, x) for x in (a, b, n))
+    eg.ecm_mulmod_batch(A, B, Nn, L=L, iters=1, flags=eg.ECM_CHECK)
+    bad = n.copy()
+    bad[0, 0] &= ~np.uint32(1)  # even modulus
+    with pytest.raises(eg.EcmError) as e:
+        eg.ecm_mulmod_batch(A, B, dev(torch, bad), L=L, iters=1, flags=eg.ECM_CHECK)
+    assert e.value.status == 2
+    big = a.copy()
+    big[0, L - 1] = 0xFFFFFFFF  # >= 2n
+    with pytest.raises(eg.EcmError) as e:
+        eg.ecm_mulmod_batch(dev(torch, big), B, Nn, L=L, iters=1, flags=eg.ECM_CHECK)
+    assert e.value.status == 5
+
+
+def test_host_buffers_path(orc, torch):
+    L = 8
+    a, b, n = mulmod_inputs(32 * 5 + 3, L, seed=9, lazy=True)
+    out = eg.ecm_mulmod_batch(a, b, n, L=L, iters=4, flags=eg.ECM_HOST_BUFFERS)
+    assert np.array_equal(out, orc.mulmod_chain(a, b, n, L, 4))
+
+
+def test_c2_full_size(orc, torch):
+    """C2: 2^24 triples, L = 6, the bench launch configuration; K = 1 and 16 element-wise,
+    K = 256 on a strided sample, out < 2N everywhere; AoS == sliced."""
+    L, count = 6, 1 << 24
+    a, b, n = mulmod_inputs(count, L, seed=2)
+    A, B, Nn = (dev(torch, x) for x in (a, b, n))
+    for iters in (1, 16):
+        got = eg.ecm_mulmod_batch(A, B, Nn, L=L, iters=iters).cpu().numpy()
+        want = orc.mulmod_chain_mt(a, b, n, L, iters)
+        assert np.array_equal(got, want), iters
+        assert lt_2n(got, n).all()
+    got = eg.ecm_mulmod_batch(A, B, Nn, L=L, iters=256).cpu().numpy()
+    assert lt_2n(got, n).all()
+    idx = np.arange(0, count, count // (1 << 14)) + 13
+    want = orc.mulmod_chain_mt(a[idx], b[idx], n[idx], L, 256)
+    assert np.array_equal(got[idx], want)
+    # the same triples in the limb-sliced layout give the same outputs
+    S = [dev(torch, x.T.copy()) for x in (a, b, n)]
+    gs = eg.ecm_mulmod_batch(*S, L=L, iters=256, flags=eg.ECM_LAYOUT_SLICED).cpu().numpy().T
+    assert np.array_equal(gs, got)
