@@ -205,6 +205,29 @@ def run_ours(args):
     achieved = fpe_launch / (kernel_ms * 1e-3)
     clocks = clk.summary()
 
+    # ---------------- square mode and the C4 width sweep (same count, K) ----------------
+    sweep = {}
+    if not args.no_sweep:
+        sq = lambda: eg.ecm_mulmod_batch(A, B, Nn, out, L=L, iters=args.iters, flags=eg.ECM_SQUARE)  # noqa: E731
+        sq()
+        ms, _ = time_steps(torch, sq, 3, ws)
+        ms = max_over_ranks(torch, ms / 3, ws)
+        fpe_sq = (3 * L * L + L) // 2
+        sweep["square_L6"] = {"modmul_per_s": count * args.iters * ws / (ms * 1e-3), "ms": ms,
+                              "frac": count * args.iters * fpe_sq / (ms * 1e-3) / pk["fpe_peak"]}
+        for Lw in (4, 8, 12):
+            aw, bw, nw = mulmod_inputs(count, Lw, seed=4, start=rank * count)
+            Aw, Bw, Nw = (torch.from_numpy(x).cuda() for x in (aw, bw, nw))
+            Ow = torch.empty_like(Aw)
+            f = lambda: eg.ecm_mulmod_batch(Aw, Bw, Nw, Ow, L=Lw, iters=args.iters)  # noqa: E731
+            f()
+            ms, _ = time_steps(torch, f, 2, ws)
+            ms = max_over_ranks(torch, ms / 2, ws)
+            sweep[f"mul_L{Lw}"] = {"bits": 32 * Lw - 2, "modmul_per_s": count * args.iters * ws / (ms * 1e-3),
+                                   "ms": ms, "frac": count * args.iters * 2 * Lw * Lw / (ms * 1e-3) / pk["fpe_peak"]}
+            del Aw, Bw, Nw, Ow
+        sweep["mul_L6"] = {"bits": 190, "modmul_per_s": value, "ms": kernel_ms, "frac": achieved / pk["fpe_peak"]}
+
     # ---------------- end to end: public API with host (pinned) buffers ----------------
     ah, bh, nh = (torch.from_numpy(x).pin_memory() for x in (a, b, n))
     oh = torch.empty_like(ah).pin_memory()
@@ -234,14 +257,11 @@ def run_ours(args):
 
         def ecm_step():
             nonlocal gathered
-            r = eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], sig, want=("g",))
             if ws > 1:
-                import torch.distributed as dist
-                gathered = torch.empty(curves, dtype=torch.uint8, device="cuda")
-                dist.all_gather_into_tensor(gathered, r["status"])
+                from paper_1310_3809_b200.dist import ecm_stage1_distributed
+                gathered, _ = ecm_stage1_distributed(cfg["N"], L, cfg["B1"], cfg["sigmas"][:curves])
             else:
-                gathered = r["status"]
-            return r
+                gathered = eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], sig, want=("g",))["status"]
 
         with ClockSampler(local) as clk2:
             ecm_ms, _ = time_steps(torch, ecm_step, 1, ws)
@@ -276,6 +296,8 @@ def run_ours(args):
     }
     if ecm:
         line["ecm"] = ecm
+    if sweep:
+        line["sweep"] = sweep
     if rank == 0 and ws == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_mulmod(args.cpu_elems, args.iters)
         if ecm:
@@ -328,6 +350,7 @@ def main():
     ap.add_argument("--no-ecm", action="store_true")
     ap.add_argument("--ecm-curves", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--cpu-elems", type=int, default=1 << 17)
     ap.add_argument("--cpu-curves", type=int, default=64)
     args = ap.parse_args()

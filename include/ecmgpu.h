@@ -56,7 +56,12 @@ typedef enum {
 #define ECM_CHECK 0x8u          /* validate per-element preconditions on the device first */
 #define ECM_HOST_BUFFERS 0x10u  /* array arguments are host pointers (see conventions) */
 #define ECM_NO_XAFF 0x20u       /* stage 1: skip the affine x (xaff may then be NULL) */
-/* REDC variant (bits 8..9): all give the SAME raw lazy value, which is a function of (T, N, R) */
+#define ECM_EAGER 0x40u         /* stage 1, ablation (L = 6, 8): canonicalise after every product and
+                                   reduce add/sub mod N — the paper's baseline without the lazy
+                                   reduction of PAPER.md:172-191.  Outputs are identical. */
+/* REDC variant (bits 8..9): all give the SAME raw lazy value, which is a function of (T, N, R).
+   Accepted by every entry point; for ecm_stage1/ladder_batch non-default variants exist for
+   L = 6 and 8 only (ECM_E_ARG otherwise). */
 #define ECM_REDC_WORD (0u << 8)     /* default: word-serial CIOS, fused IMAD.WIDE carry chains */
 #define ECM_REDC_KNOWNLOW (1u << 8) /* the paper's Theorem per word: lo(m_i N_0) = -t_0 not multiplied */
 #define ECM_REDC_BLOCKTHM (2u << 8) /* block SOS with the Theorem: 3 of 4 quadrant products of q*N */

@@ -26,7 +26,7 @@ namespace {
 using ecm::EcmParams;
 
 constexpr uint32_t kKnownFlags = ECM_CANONICAL | ECM_SQUARE | ECM_LAYOUT_SLICED | ECM_CHECK | ECM_HOST_BUFFERS |
-                                 ECM_NO_XAFF | ECM_REDC_MASK;
+                                 ECM_NO_XAFF | ECM_EAGER | ECM_REDC_MASK;
 
 bool valid_L(int L) { return L == 4 || L == 6 || L == 8 || L == 12; }
 
@@ -83,6 +83,18 @@ ecm_status make_params(EcmParams& p, const uint32_t* N, int L) {
   uint32_t x = N[0];  // correct to 3 bits
   for (int i = 0; i < 5; ++i) x *= 2u - N[0] * x;
   p.n0inv = 0u - x;
+  // -N^{-1} mod R word by word: choose word i of X so that word i of N*X is 0xffffffff
+  std::vector<uint64_t> S(L + 1, 0);
+  for (int i = 0; i < L; ++i) {
+    const uint32_t xi = (uint32_t)((0xffffffffull - S[i]) & 0xffffffffull) * p.n0inv * 0xffffffffu;  // * N0^{-1}
+    p.NP[i] = xi;
+    uint64_t c = 0;
+    for (int j = 0; i + j < L; ++j) {
+      const uint64_t t = S[i + j] + (uint64_t)xi * N[j] + c;
+      S[i + j] = t & 0xffffffffull;
+      c = t >> 32;
+    }
+  }
   return ECM_OK;
 }
 
@@ -126,10 +138,29 @@ ecm_status cuda_err(cudaError_t e) {
   return ECM_E_CUDA;
 }
 
+// ablation variants of the ECM kernel exist for L = 6 and 8 only (csrc/ecm.cu)
+bool ecm_variant_ok(int L, uint32_t flags) {
+  const bool ablation = (flags & ECM_REDC_MASK) || (flags & ECM_EAGER);
+  return !ablation || L == 6 || L == 8;
+}
+
 bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
 
+// Stream-ordered scratch from the device's default memory pool.  The pool keeps freed memory
+// (release threshold = max) so repeated ECM_HOST_BUFFERS calls do not re-map pages each time.
 template <class T>
 cudaError_t dev_alloc(T** p, size_t bytes, cudaStream_t s) {
+  static std::once_flag once[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64) {
+    std::call_once(once[dev], [dev] {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+    });
+  }
   return cudaMallocAsync(reinterpret_cast<void**>(p), bytes, s);
 }
 
@@ -172,6 +203,54 @@ ecm_status run_ecm(const uint32_t* N_host, int L, const uint32_t* kw_dev, uint32
   return cuda_err(e);
 }
 
+// ECM_HOST_BUFFERS without ECM_CHECK, AoS layout: the batch is cut into chunks that cycle
+// through two internal streams, so the host->device copy of chunk c+1, the kernel of chunk c and
+// the device->host copy of chunk c-1 overlap (copy engines and SMs run concurrently).
+cudaError_t mulmod_host_pipelined(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out,
+                                  size_t count, int L, uint32_t iters, uint32_t flags, cudaStream_t s) {
+  const bool square = flags & ECM_SQUARE;
+  size_t chunk = (count + 7) / 8;
+  if (chunk < ((size_t)1 << 18)) chunk = (size_t)1 << 18;
+  chunk = (chunk + 31) / 32 * 32;
+  const size_t cw = chunk * (size_t)L;  // words per array per slot
+  uint32_t* scratch = nullptr;
+  cudaError_t e = dev_alloc(&scratch, 2 * 4 * cw * sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaEvent_t start = nullptr, done[2] = {nullptr, nullptr};
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(start, s);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(st[i], start, 0);
+  for (size_t c0 = 0, c = 0; c0 < count && e == cudaSuccess; c0 += chunk, ++c) {
+    const size_t m = (count - c0) < chunk ? (count - c0) : chunk;
+    const size_t by = m * (size_t)L * sizeof(uint32_t);
+    cudaStream_t q = st[c & 1];
+    uint32_t* base = scratch + (c & 1) * 4 * cw;
+    uint32_t *ta = base, *tb = base + cw, *tn = base + 2 * cw, *to = base + 3 * cw;
+    e = cudaMemcpyAsync(ta, a + c0 * L, by, cudaMemcpyHostToDevice, q);
+    if (e == cudaSuccess && !square) e = cudaMemcpyAsync(tb, b + c0 * L, by, cudaMemcpyHostToDevice, q);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(tn, n + c0 * L, by, cudaMemcpyHostToDevice, q);
+    if (e == cudaSuccess) e = ecm::launch_mulmod(ta, square ? nullptr : tb, tn, to, m, L, iters, flags, q);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out + c0 * L, to, by, cudaMemcpyDeviceToHost, q);
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (done[i] && st[i]) {
+      cudaEventRecord(done[i], st[i]);
+      cudaStreamWaitEvent(s, done[i], 0);
+    }
+  }
+  cudaFreeAsync(scratch, s);
+  const cudaError_t e2 = cudaStreamSynchronize(s);
+  for (int i = 0; i < 2; ++i) {
+    if (st[i]) cudaStreamDestroy(st[i]);
+    if (done[i]) cudaEventDestroy(done[i]);
+  }
+  if (start) cudaEventDestroy(start);
+  return e != cudaSuccess ? e : e2;
+}
+
 }  // namespace
 
 extern "C" {
@@ -204,7 +283,7 @@ ecm_status ecm_mulmod_batch(const uint32_t* a, const uint32_t* b, const uint32_t
   const bool square = flags & ECM_SQUARE;
   if (!a || !n || !out || (!b && !square) || count == 0 || !valid_L(L) || iters == 0 || (flags & ~kKnownFlags))
     return ECM_E_ARG;
-  if (flags & ECM_NO_XAFF) return ECM_E_ARG;
+  if (flags & (ECM_NO_XAFF | ECM_EAGER)) return ECM_E_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool host = flags & ECM_HOST_BUFFERS;
   const size_t bytes = count * (size_t)L * sizeof(uint32_t);
@@ -214,6 +293,8 @@ ecm_status ecm_mulmod_batch(const uint32_t* a, const uint32_t* b, const uint32_t
   uint32_t* dout = out;
   uint8_t* scratch = nullptr;
   cudaError_t e = cudaSuccess;
+  if (host && !(flags & (ECM_CHECK | ECM_LAYOUT_SLICED)))
+    return cuda_err(mulmod_host_pipelined(a, b, n, out, count, L, iters, flags, s));
   if (host) {
     e = dev_alloc(&scratch, 4 * bytes + 16, s);
     if (e != cudaSuccess) return cuda_err(e);
@@ -258,7 +339,8 @@ ecm_status ecm_stage1_batch(const uint32_t* N_host, int L, uint64_t B1, const ui
                             uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status, uint32_t* xaff, uint32_t flags,
                             void* stream) {
   if (!N_host || !sigmas || !status || count == 0 || !valid_L(L) || (flags & ~kKnownFlags)) return ECM_E_ARG;
-  if (flags & (ECM_SQUARE | ECM_LAYOUT_SLICED | ECM_CANONICAL | ECM_REDC_MASK)) return ECM_E_ARG;
+  if (flags & (ECM_SQUARE | ECM_LAYOUT_SLICED | ECM_CANONICAL)) return ECM_E_ARG;
+  if (!ecm_variant_ok(L, flags)) return ECM_E_ARG;
   if (!xaff && !(flags & ECM_NO_XAFF)) flags |= ECM_NO_XAFF;
   if (B1 < 2 || B1 >= (1ull << 32)) return ECM_E_B1;
   EcmParams probe;
@@ -292,7 +374,8 @@ ecm_status ecm_ladder_batch(const uint32_t* N_host, int L, const uint32_t* k_wor
                             uint8_t* status, uint32_t* xaff, uint32_t flags, void* stream) {
   if (!N_host || !k_words || !sigmas || !status || count == 0 || !valid_L(L) || (flags & ~kKnownFlags))
     return ECM_E_ARG;
-  if (flags & (ECM_SQUARE | ECM_LAYOUT_SLICED | ECM_CANONICAL | ECM_REDC_MASK)) return ECM_E_ARG;
+  if (flags & (ECM_SQUARE | ECM_LAYOUT_SLICED | ECM_CANONICAL)) return ECM_E_ARG;
+  if (!ecm_variant_ok(L, flags)) return ECM_E_ARG;
   if (!xaff && !(flags & ECM_NO_XAFF)) flags |= ECM_NO_XAFF;
   if (k_bits == 0) return ECM_E_B1;
   const size_t nw = (k_bits + 31) / 32;

@@ -151,35 +151,66 @@ __device__ bool xgcd(const uint32_t (&a)[L], const uint32_t (&N)[L], uint32_t (&
 }
 
 // ---------------------------------------------------------------------------------------
+// Field products of the ladder, templated for the paper's ablation (Table 5 analogue, §8(f) N1):
+//   V     : REDC variant (mont.cuh); all give the same raw value.
+//   EAGER : canonicalise after every product and reduce add/sub modulo N (the "without
+//           Section 2.2" baseline: 18 conditional reductions per step instead of 8).
+// ---------------------------------------------------------------------------------------
+template <int L, int V, bool EAGER>
+struct Field {
+  const uint32_t (&N)[L];
+  const uint32_t (&M)[L];   // add/sub modulus: 2N (lazy) or N (eager)
+  const uint32_t (&NP)[L];  // -N^{-1} mod R (block variants)
+  uint32_t n0inv;
+  __device__ __forceinline__ void mul(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L]) const {
+    if (V == REDC_WORD || V == REDC_KNOWNLOW) mont_mul_cios<L, V>(r, x, y, N, n0inv);
+    else mont_mul_block<L, V>(r, x, y, N, NP);
+    if (EAGER) canonicalize<L>(r, r, N);
+  }
+  __device__ __forceinline__ void sqr(uint32_t (&r)[L], const uint32_t (&x)[L]) const {
+    if (V == REDC_WORD) mont_sqr<L>(r, x, N, n0inv);
+    else if (V == REDC_KNOWNLOW) mont_mul_cios<L, V>(r, x, x, N, n0inv);
+    else mont_mul_block<L, V>(r, x, x, N, NP);
+    if (EAGER) canonicalize<L>(r, r, N);
+  }
+  __device__ __forceinline__ void add(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L]) const {
+    add_lazy<L>(r, x, y, M);
+  }
+  __device__ __forceinline__ void sub(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L]) const {
+    sub_lazy<L>(r, x, y, M);
+  }
+};
+
+// ---------------------------------------------------------------------------------------
 // One combined ladder step on (X0:Z0) [doubled] and (X1:Z1) [added], difference (x0:1):
 //   t1 = X0+Z0, t2 = X0-Z0, t3 = X1+Z1, t4 = X1-Z1
 //   U = t2 t3, V = t1 t4, s = t1^2, d = t2^2
 //   X0' = s d,  t = s - d,  Z0' = t (d + a24 t)
 //   X1' = (U+V)^2,  Z1' = x0 (U-V)^2
 // ---------------------------------------------------------------------------------------
-template <int L>
+template <int L, class F>
 __device__ __forceinline__ void ladder_step(uint32_t (&X0)[L], uint32_t (&Z0)[L], uint32_t (&X1)[L],
                                             uint32_t (&Z1)[L], const uint32_t (&x0)[L], const uint32_t (&a24)[L],
-                                            const uint32_t (&N)[L], const uint32_t (&N2)[L], uint32_t n0inv) {
+                                            const F& f) {
   uint32_t t1[L], t2[L], t3[L], t4[L], U[L], V[L], s[L], d[L];
-  add_lazy<L>(t1, X0, Z0, N2);
-  sub_lazy<L>(t2, X0, Z0, N2);
-  add_lazy<L>(t3, X1, Z1, N2);
-  sub_lazy<L>(t4, X1, Z1, N2);
-  mont_mul<L>(U, t2, t3, N, n0inv);
-  mont_mul<L>(V, t1, t4, N, n0inv);
-  mont_mul<L>(s, t1, t1, N, n0inv);
-  mont_mul<L>(d, t2, t2, N, n0inv);
-  mont_mul<L>(X0, s, d, N, n0inv);
-  sub_lazy<L>(t1, s, d, N2);            // t
-  mont_mul<L>(t2, a24, t1, N, n0inv);   // a24 t
-  add_lazy<L>(t2, d, t2, N2);           // d + a24 t
-  mont_mul<L>(Z0, t1, t2, N, n0inv);
-  add_lazy<L>(t3, U, V, N2);
-  sub_lazy<L>(t4, U, V, N2);
-  mont_mul<L>(X1, t3, t3, N, n0inv);
-  mont_mul<L>(t4, t4, t4, N, n0inv);
-  mont_mul<L>(Z1, x0, t4, N, n0inv);
+  f.add(t1, X0, Z0);
+  f.sub(t2, X0, Z0);
+  f.add(t3, X1, Z1);
+  f.sub(t4, X1, Z1);
+  f.mul(U, t2, t3);
+  f.mul(V, t1, t4);
+  f.sqr(s, t1);
+  f.sqr(d, t2);
+  f.mul(X0, s, d);
+  f.sub(t1, s, d);   // t
+  f.mul(t2, a24, t1); // a24 t
+  f.add(t2, d, t2);  // d + a24 t
+  f.mul(Z0, t1, t2);
+  f.add(t3, U, V);
+  f.sub(t4, U, V);
+  f.sqr(X1, t3);
+  f.sqr(t4, t4);
+  f.mul(Z1, x0, t4);
 }
 
 template <int L>
@@ -201,7 +232,7 @@ __device__ __forceinline__ void store(uint32_t* dst, size_t i, const uint32_t (&
   for (int k = 0; k < L / 2; ++k) d2[k] = make_uint2(v[2 * k], v[2 * k + 1]);
 }
 
-template <int L>
+template <int L, int VAR, bool EAGER>
 __global__ void __launch_bounds__(kEcmTPB) ecm_stage1_kernel(const __grid_constant__ EcmParams p,
                                                              const uint32_t* __restrict__ kwords, uint32_t k_bits,
                                                              const uint64_t* __restrict__ sigmas, size_t count,
@@ -211,7 +242,9 @@ __global__ void __launch_bounds__(kEcmTPB) ecm_stage1_kernel(const __grid_consta
   const uint32_t(&N2)[L] = cref<L>(p.N2);
   const uint32_t(&R2)[L] = cref<L>(p.R2);
   const uint32_t(&ONE)[L] = cref<L>(p.ONE);
+  const uint32_t(&NP)[L] = cref<L>(p.NP);
   const uint32_t n0inv = p.n0inv;
+  const Field<L, VAR, EAGER> fld{N, EAGER ? N : N2, NP, n0inv};
   const int lane = threadIdx.x & 31;
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = i < count;
@@ -279,20 +312,24 @@ __global__ void __launch_bounds__(kEcmTPB) ecm_stage1_kernel(const __grid_consta
   }
 
   // ---------------- ladder over k (warp-uniform bits) ----------------
+  if (EAGER) {
+    canonicalize<L>(x0, x0, N);
+    canonicalize<L>(a24, a24, N);
+  }
   copy(X0, x0);
   copy(Z0, ONE);
   {
-    // R1 = xDBL(P): reuse the step with a dummy second point (its outputs are overwritten)
+    // R1 = xDBL(P)
     uint32_t t1[L], t2[L], sd[L], dd[L], tt[L];
-    add_lazy<L>(t1, X0, Z0, N2);
-    sub_lazy<L>(t2, X0, Z0, N2);
-    mont_mul<L>(sd, t1, t1, N, n0inv);
-    mont_mul<L>(dd, t2, t2, N, n0inv);
-    mont_mul<L>(X1, sd, dd, N, n0inv);
-    sub_lazy<L>(tt, sd, dd, N2);
-    mont_mul<L>(t1, a24, tt, N, n0inv);
-    add_lazy<L>(t1, dd, t1, N2);
-    mont_mul<L>(Z1, tt, t1, N, n0inv);
+    fld.add(t1, X0, Z0);
+    fld.sub(t2, X0, Z0);
+    fld.sqr(sd, t1);
+    fld.sqr(dd, t2);
+    fld.mul(X1, sd, dd);
+    fld.sub(tt, sd, dd);
+    fld.mul(t1, a24, tt);
+    fld.add(t1, dd, t1);
+    fld.mul(Z1, tt, t1);
   }
   bool swapped = false;
   if (k_bits >= 2) {
@@ -311,7 +348,7 @@ __global__ void __launch_bounds__(kEcmTPB) ecm_stage1_kernel(const __grid_consta
       cswap<L>(X0, X1, bit != swapped);
       cswap<L>(Z0, Z1, bit != swapped);
       swapped = bit;
-      ladder_step<L>(X0, Z0, X1, Z1, x0, a24, N, N2, n0inv);
+      ladder_step<L>(X0, Z0, X1, Z1, x0, a24, fld);
     }
   }
   cswap<L>(X0, X1, swapped);
@@ -351,14 +388,38 @@ __global__ void __launch_bounds__(kEcmTPB) ecm_stage1_kernel(const __grid_consta
   status[i] = st;
 }
 
+template <int L, int VAR, bool EAGER>
+static cudaError_t launch_ecm_LV(const EcmParams& p, const uint32_t* kw, uint32_t k_bits, const uint64_t* sigmas,
+                                 size_t count, uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status, uint32_t* xaff,
+                                 uint32_t flags, cudaStream_t s) {
+  const size_t blocks = (count + kEcmTPB - 1) / kEcmTPB;
+  ecm_stage1_kernel<L, VAR, EAGER><<<(unsigned)blocks, kEcmTPB, 0, s>>>(p, kw, k_bits, sigmas, count, X, Z, g,
+                                                                        status, xaff, flags);
+  return cudaGetLastError();
+}
+
+// Ablation variants (REDC form x eager/lazy) are instantiated for L = 6 and 8 (192/256-bit,
+// the paper's 254-bit setting); every width gets the default lazy word-serial kernel.
 template <int L>
 static cudaError_t launch_ecm_L(const EcmParams& p, const uint32_t* kw, uint32_t k_bits, const uint64_t* sigmas,
                                 size_t count, uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status, uint32_t* xaff,
                                 uint32_t flags, cudaStream_t s) {
-  const size_t blocks = (count + kEcmTPB - 1) / kEcmTPB;
-  ecm_stage1_kernel<L><<<(unsigned)blocks, kEcmTPB, 0, s>>>(p, kw, k_bits, sigmas, count, X, Z, g, status, xaff,
-                                                            flags);
-  return cudaGetLastError();
+  const uint32_t var = (flags >> 8) & 3u;
+  const bool eager = flags & 0x40u;
+  if (var == REDC_WORD && !eager) return launch_ecm_LV<L, REDC_WORD, false>(p, kw, k_bits, sigmas, count, X, Z, g, status, xaff, flags, s);
+  if constexpr (L == 6 || L == 8) {
+#define ECM_CASE(V, E) \
+    if (var == V && eager == E) return launch_ecm_LV<L, V, E>(p, kw, k_bits, sigmas, count, X, Z, g, status, xaff, flags, s);
+    ECM_CASE(REDC_WORD, true)
+    ECM_CASE(REDC_KNOWNLOW, false)
+    ECM_CASE(REDC_KNOWNLOW, true)
+    ECM_CASE(REDC_BLOCKTHM, false)
+    ECM_CASE(REDC_BLOCKTHM, true)
+    ECM_CASE(REDC_CLASSIC, false)
+    ECM_CASE(REDC_CLASSIC, true)
+#undef ECM_CASE
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_ecm(const EcmParams& p, const uint32_t* kw, uint32_t k_bits, const uint64_t* sigmas, size_t count,

@@ -18,7 +18,7 @@ cudaError_t launch_mulmod_check(const uint32_t* a, const uint32_t* b, const uint
 struct EcmParams {
   int L;
   uint32_t n0inv;
-  uint32_t N[16], N2[16], R2[16], ONE[16];  // N, 2N, R^2 mod N, R mod N (Montgomery 1)
+  uint32_t N[16], N2[16], R2[16], ONE[16], NP[16];  // N, 2N, R^2 mod N, R mod N (Montgomery 1), -N^{-1} mod R
 };
 
 cudaError_t launch_ecm(const EcmParams& p, const uint32_t* kbits_dev, uint32_t k_bits, const uint64_t* sigmas,

@@ -249,6 +249,125 @@ __device__ __forceinline__ void mont_mul_block(uint32_t (&r)[L], const uint32_t 
 }
 
 // ------------------------------------------------------------------------------------------
+// Lazy Montgomery squaring: the same unique raw value as mont_mul_cios(x, x), with
+// (3L^2 + L)/2 partial products instead of 2L^2.
+//   T = x^2 = sum_r x_r * V_r * 2^(64r),  V_r = [x_r, 2x_{r+1}, 2x_{r+2}, ...] taken from
+//   Y = 2x (fits L words because x < 2N < 2^(32L-1)); word r+1 of Y carries bit 31 of x_r,
+//   which does not belong to row r and is masked off.  Row r = L-r products at offset 2r.
+//   Even/odd product offsets go to accumulators EV/OD (disjoint pairs -> one carry chain
+//   each); rows run in increasing r, so each chain's carry lands in a word that so far holds
+//   only earlier carries and is absorbed by one add, never rippled.
+//   Reduction: the even/odd CIOS frame of mont_mul_cios on T mod R, plus T's high half.
+// ------------------------------------------------------------------------------------------
+template <int L>
+__device__ __forceinline__ void mont_sqr(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&n)[L], uint32_t n0inv) {
+  static_assert(L % 2 == 0 && L >= 2, "L must be even");
+  uint32_t Y[L];
+  Y[0] = x[0] << 1;
+#pragma unroll
+  for (int k = 1; k < L; ++k) Y[k] = __funnelshift_l(x[k - 1], x[k], 1);
+  uint32_t EV[2 * L + 1], OD[2 * L + 1];
+#pragma unroll
+  for (int k = 0; k <= 2 * L; ++k) { EV[k] = 0; OD[k] = 0; }
+#pragma unroll
+  for (int row = 0; row < L; ++row) {
+    const uint32_t xr = x[row];
+    // even k -> EV pairs (2row+k, 2row+k+1)
+#pragma unroll
+    for (int k = 0; k < L - row; k += 2) {
+      const uint32_t v = (k == 0) ? xr : Y[row + k];
+      const int w = 2 * row + k;
+      if (k == 0) EV[w] = ptx::mad_lo_cc(xr, v, EV[w]);
+      else EV[w] = ptx::madc_lo_cc(xr, v, EV[w]);
+      EV[w + 1] = ptx::madc_hi_cc(xr, v, EV[w + 1]);
+    }
+    {
+      const int klast = ((L - row - 1) / 2) * 2;
+      const int w = 2 * row + klast + 2;
+      EV[w] = ptx::addc(EV[w], 0u);
+    }
+    // odd k -> OD pairs
+    if (L - row > 1) {
+#pragma unroll
+      for (int k = 1; k < L - row; k += 2) {
+        const uint32_t v = (k == 1) ? (Y[row + 1] & 0xfffffffeu) : Y[row + k];
+        const int w = 2 * row + k;
+        if (k == 1) OD[w] = ptx::mad_lo_cc(xr, v, OD[w]);
+        else OD[w] = ptx::madc_lo_cc(xr, v, OD[w]);
+        OD[w + 1] = ptx::madc_hi_cc(xr, v, OD[w + 1]);
+      }
+      const int klast = ((L - row - 2) / 2) * 2 + 1;
+      const int w = 2 * row + klast + 2;
+      OD[w] = ptx::addc(OD[w], 0u);
+    }
+  }
+  // T = EV + OD (< 2^(64L): the top carry and EV/OD[2L] are zero)
+  uint32_t T[2 * L];
+  T[0] = EV[0];
+  T[1] = ptx::add_cc(EV[1], OD[1]);
+#pragma unroll
+  for (int k = 2; k < 2 * L - 1; ++k) T[k] = ptx::addc_cc(EV[k], OD[k]);
+  T[2 * L - 1] = ptx::addc(EV[2 * L - 1], OD[2 * L - 1]);
+  // Word-serial reduction of T_low = T mod R in the even/odd frame of mont_mul_cios (E =
+  // T_low, O = 0, no product rows), then r = (T_low + q N)/R + T_high: q depends only on
+  // T mod R, so this is exactly (T + q N)/R.  (T_low + qN)/R < N + 1, so the window bounds
+  // of mont_mul_cios hold and the final sum is the unique raw value < 2N.
+  uint32_t E[L], O[L];
+#pragma unroll
+  for (int k = 0; k < L; ++k) { E[k] = T[k]; O[k] = 0; }
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    const uint32_t m = E[0] * n0inv;
+    if (i == 0) chain<L, 1, false, false>(O, O, m, n);
+    else chain<L, 1, true, false>(O, O, m, n);
+    chain<L, 0, false, true>(E, E, m, n);
+    O[L - 1] = ptx::addc(O[L - 1], 0u);
+    uint32_t nE[L], nO[L];
+#pragma unroll
+    for (int k = 0; k < L; ++k) nE[k] = O[k];
+    nE[0] = ptx::add_cc(nE[0], E[1]);
+#pragma unroll
+    for (int k = 0; k < L; ++k) nO[k] = (k + 2 < L) ? E[k + 2] : 0u;
+#pragma unroll
+    for (int k = 0; k < L; ++k) { E[k] = nE[k]; O[k] = nO[k]; }
+  }
+  uint32_t q[L];
+  q[0] = E[0];
+#pragma unroll
+  for (int k = 1; k < L - 1; ++k) q[k] = ptx::addc_cc(E[k], O[k - 1]);
+  q[L - 1] = ptx::addc(E[L - 1], O[L - 2]);
+  r[0] = ptx::add_cc(q[0], T[L]);
+#pragma unroll
+  for (int k = 1; k < L - 1; ++k) r[k] = ptx::addc_cc(q[k], T[L + k]);
+  r[L - 1] = ptx::addc(q[L - 1], T[2 * L - 1]);
+}
+
+// -N^{-1} mod R over the full width, for the block (SOS) REDC variants: Newton lifting
+// x <- x (2 - N x) of N^{-1} from the 32-bit inverse, doubling the correct words.
+template <int L>
+__device__ __forceinline__ void nprime_full(uint32_t (&np)[L], const uint32_t (&n)[L]) {
+  uint32_t x[L];
+#pragma unroll
+  for (int k = 0; k < L; ++k) x[k] = 0;
+  x[0] = 0u - neg_inv32(n[0]);  // N^{-1} mod 2^32
+#pragma unroll
+  for (int correct = 1; correct < L; correct *= 2) {
+    uint32_t t[L], u[L];
+    mul_low_half<L>(t, n, x);  // t = N x
+    // u = 2 - t  (mod R)
+    u[0] = ptx::sub_cc(2u, t[0]);
+#pragma unroll
+    for (int k = 1; k < L; ++k) u[k] = ptx::subc_cc(0u, t[k]);
+    mul_low_half<L>(t, x, u);
+#pragma unroll
+    for (int k = 0; k < L; ++k) x[k] = t[k];
+  }
+  np[0] = ptx::sub_cc(0u, x[0]);
+#pragma unroll
+  for (int k = 1; k < L; ++k) np[k] = ptx::subc_cc(0u, x[k]);
+}
+
+// ------------------------------------------------------------------------------------------
 // Lazy add / sub in [0, 2N) with a precomputed 2N: both candidates
 // are formed and the carry/borrow bit selects — no data-dependent branch.
 // ------------------------------------------------------------------------------------------

@@ -18,31 +18,6 @@ namespace ecm {
 
 constexpr int kMulmodTPB = 256;
 
-// -N^{-1} mod R over the full width, for the block (SOS) REDC variants: Newton lifting
-// x <- x (2 - N x) of N^{-1} from the 32-bit inverse, doubling the correct words.
-template <int L>
-__device__ __forceinline__ void nprime_full(uint32_t (&np)[L], const uint32_t (&n)[L]) {
-  uint32_t x[L];
-#pragma unroll
-  for (int k = 0; k < L; ++k) x[k] = 0;
-  x[0] = 0u - neg_inv32(n[0]);  // N^{-1} mod 2^32
-#pragma unroll
-  for (int correct = 1; correct < L; correct *= 2) {
-    uint32_t t[L], u[L];
-    mul_low_half<L>(t, n, x);  // t = N x
-    // u = 2 - t  (mod R)
-    u[0] = ptx::sub_cc(2u, t[0]);
-#pragma unroll
-    for (int k = 1; k < L; ++k) u[k] = ptx::subc_cc(0u, t[k]);
-    mul_low_half<L>(t, x, u);
-#pragma unroll
-    for (int k = 0; k < L; ++k) x[k] = t[k];
-  }
-  np[0] = ptx::sub_cc(0u, x[0]);
-#pragma unroll
-  for (int k = 1; k < L; ++k) np[k] = ptx::subc_cc(0u, x[k]);
-}
-
 // Warp-cooperative AoS tile load: words [e0*L, e0*L + nvalid*L) -> smem tile, then lane's L words.
 template <int L>
 __device__ __forceinline__ void load_aos(uint32_t (&v)[L], const uint32_t* __restrict__ g, uint32_t* tile,
@@ -132,7 +107,8 @@ __global__ void __launch_bounds__(kMulmodTPB) mulmod_batch_kernel(const uint32_t
     for (uint32_t t = 0; t < iters; ++t) {
       uint32_t r[L];
       if (V == REDC_WORD || V == REDC_KNOWNLOW) {
-        if (SQUARE) mont_mul_cios<L, V>(r, x, x, nn, n0inv);
+        if (SQUARE && V == REDC_WORD) mont_sqr<L>(r, x, nn, n0inv);
+        else if (SQUARE) mont_mul_cios<L, V>(r, x, x, nn, n0inv);
         else mont_mul_cios<L, V>(r, x, y, nn, n0inv);
       } else {
         if (SQUARE) mont_mul_block<L, V>(r, x, x, nn, np);

@@ -157,3 +157,17 @@ def test_c2_full_size(orc, torch):
     S = [dev(torch, x.T.copy()) for x in (a, b, n)]
     gs = eg.ecm_mulmod_batch(*S, L=L, iters=256, flags=eg.ECM_LAYOUT_SLICED).cpu().numpy().T
     assert np.array_equal(gs, got)
+
+
+def test_host_buffers_pipelined_multichunk(orc, torch):
+    """ECM_HOST_BUFFERS splits large batches into chunks over two internal streams."""
+    L = 4
+    count = (1 << 19) + 77
+    a, b, n = mulmod_inputs(count, L, seed=10, lazy=True)
+    ap, bp, np_ = (torch.from_numpy(x).pin_memory() for x in (a, b, n))
+    out = torch.empty_like(ap).pin_memory()
+    eg.ecm_mulmod_batch(ap, bp, np_, out, L=L, iters=3, flags=eg.ECM_HOST_BUFFERS)
+    want = orc.mulmod_chain_mt(a, b, n, L, 3)
+    assert np.array_equal(out.numpy(), want)
+    sq = eg.ecm_mulmod_batch(a, b, n, L=L, iters=2, flags=eg.ECM_HOST_BUFFERS | eg.ECM_SQUARE)
+    assert np.array_equal(sq, orc.mulmod_chain_mt(a, b, n, L, 2, square=True))

@@ -1,0 +1,35 @@
+#!/usr/bin/env python3
+"""Single-launch drivers for ncu captures (tools/profile.sh).  Not a benchmark: numbers taken
+under a profiler are never reported as bench values."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_1310_3809_b200 as eg  # noqa: E402
+from workload import ecm_config, mulmod_inputs  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("what", choices=["mulmod", "ecm"])
+ap.add_argument("--L", type=int, default=6)
+ap.add_argument("--count", type=int, default=1 << 24)
+ap.add_argument("--iters", type=int, default=256)
+ap.add_argument("--flags", type=int, default=0)
+ap.add_argument("--curves", type=int, default=1 << 16)
+ap.add_argument("--B1", type=int, default=50000)
+ap.add_argument("--reps", type=int, default=2)
+a = ap.parse_args()
+torch.cuda.set_device(0)
+if a.what == "mulmod":
+    x, y, n = (torch.from_numpy(v).cuda() for v in mulmod_inputs(a.count, a.L, seed=2))
+    for _ in range(a.reps):
+        eg.ecm_mulmod_batch(x, y, n, L=a.L, iters=a.iters, flags=a.flags)
+else:
+    cfg = ecm_config("C3")
+    s = torch.from_numpy(cfg["sigmas"][: a.curves].copy()).cuda()
+    for _ in range(a.reps):
+        eg.ecm_stage1_batch(cfg["N"], 6, a.B1, s, want=("g",))
+torch.cuda.synchronize()
+print("done")
