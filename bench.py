@@ -277,6 +277,26 @@ def run_ours(args):
                             "frac": curves_s / ws * fpe_curve / pk["fpe_peak"]},
                "clocks": clk2.summary()}
 
+    # ---------------- optional: one rank's shard of C5 (8-GPU config) on this GPU ----------------
+    c5 = None
+    if args.c5:
+        cfg5 = ecm_config("C5")
+        per_rank = cfg5["curves"] // 8
+        lo = rank * per_rank
+        sig5 = torch.from_numpy(cfg5["sigmas"][lo:lo + per_rank].copy()).cuda()
+        kb5 = eg.ecm_stage1_kbits(cfg5["B1"])
+        eg.ecm_stage1_batch(cfg5["N"], 8, cfg5["B1"], sig5[:1024], want=("g",))
+        r5 = {}
+        with ClockSampler(local) as clk5:
+            ms5, _ = time_steps(torch, lambda: r5.update(eg.ecm_stage1_batch(cfg5["N"], 8, cfg5["B1"], sig5,
+                                                                                 want=("g",))), 1, ws)
+        cps5 = per_rank / (ms5 * 1e-3)
+        fpe5 = (kb5 - 1) * (18 * 64 + 16)
+        c5 = {"workload": f"C5 rank shard: {per_rank} of 2^22 curves, B1={cfg5['B1']}, 254-bit N (planted 80-bit p)",
+              "curves_per_s_per_gpu": cps5, "ms": ms5, "k_bits": kb5,
+              "flagged_factor": int((r5["status"] == 1).sum().item()),
+              "frac": cps5 * fpe5 / pk["fpe_peak"], "clocks": clk5.summary()}
+
     line = {
         "metric": "192-bit Montgomery modmul/s",
         "value": value, "unit": "modmul/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -298,6 +318,8 @@ def run_ours(args):
         line["ecm"] = ecm
     if sweep:
         line["sweep"] = sweep
+    if c5:
+        line["c5_shard"] = c5
     if rank == 0 and ws == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_mulmod(args.cpu_elems, args.iters)
         if ecm:
@@ -351,6 +373,7 @@ def main():
     ap.add_argument("--ecm-curves", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--c5", action="store_true", help="also time one rank's 1/8 shard of C5 (~40 s)")
     ap.add_argument("--cpu-elems", type=int, default=1 << 17)
     ap.add_argument("--cpu-curves", type=int, default=64)
     args = ap.parse_args()

@@ -59,6 +59,11 @@ typedef enum {
 #define ECM_EAGER 0x40u         /* stage 1, ablation (L = 6, 8): canonicalise after every product and
                                    reduce add/sub mod N — the paper's baseline without the lazy
                                    reduction of PAPER.md:172-191.  Outputs are identical. */
+#define ECM_PRIME_LADDERS 0x80u /* stage 1 (L = 6, 8): the paper-comparable schedule (G9b) —
+                                   Q <- [p]Q for every prime p <= B1 ascending, each e_p times, by
+                                   ladders with a projective difference (11 products per step)
+                                   instead of one ladder over k.  Same [k]P, status and affine x;
+                                   X and Z differ by a projective factor. */
 /* REDC variant (bits 8..9): all give the SAME raw lazy value, which is a function of (T, N, R).
    Accepted by every entry point; for ecm_stage1/ladder_batch non-default variants exist for
    L = 6 and 8 only (ECM_E_ARG otherwise). */

@@ -57,6 +57,9 @@ def lib():
         L.orc_ecm_stage1.argtypes = [_u32p, ctypes.c_int, _u32p, ctypes.c_uint32, _u64p, ctypes.c_size_t,
                                      _u32p, _u32p, _u32p, _u8p, _u32p]
         L.orc_ecm_stage1.restype = ctypes.c_int
+        L.orc_ecm_stage1_primes.argtypes = [_u32p, ctypes.c_int, ctypes.c_uint64, _u64p, ctypes.c_size_t,
+                                            _u32p, _u32p, _u32p, _u8p, _u32p]
+        L.orc_ecm_stage1_primes.restype = ctypes.c_int
         L.orc_suyama.argtypes = [_u32p, ctypes.c_int, ctypes.c_uint64, _u32p, _u32p, _u32p]
         L.orc_suyama.restype = ctypes.c_int
         L.orc_ladder_trace.argtypes = [_u32p, ctypes.c_int, _u32p, ctypes.c_uint32, ctypes.c_uint64, _u32p]
@@ -176,6 +179,19 @@ def ecm_stage1(N: int, L: int, k: int, sigmas, want_xaff: bool = True):
     return {"X": X, "Z": Z, "g": g, "status": st, "xaff": xa}
 
 
+def ecm_stage1_primes(N: int, L: int, B1: int, sigmas):
+    """Paper-comparable schedule: prime-by-prime ladders (see oracle.h)."""
+    sig = np.ascontiguousarray(np.asarray(sigmas, dtype=np.uint64))
+    count = sig.size
+    Nl = to_limbs(N, L)
+    X, Z, g, xa = (np.zeros((count, L), np.uint32) for _ in range(4))
+    st = np.zeros(count, np.uint8)
+    rc = lib().orc_ecm_stage1_primes(_p(Nl), L, B1, _p(sig, _u64p), count, _p(X), _p(Z), _p(g), _p(st, _u8p), _p(xa))
+    if rc != 0:
+        raise ValueError("orc_ecm_stage1_primes: bad arguments")
+    return {"X": X, "Z": Z, "g": g, "status": st, "xaff": xa}
+
+
 def suyama(N: int, L: int, sigma: int):
     x0 = np.zeros(L, np.uint32)
     a24 = np.zeros(L, np.uint32)
@@ -217,6 +233,16 @@ def mulmod_chain_mt(a, b, n, L, iters, square=False, canonical=False, threads=No
     parts = _pool_map(lambda r: mulmod_chain(a[r[0]:r[1]], b[r[0]:r[1]], n[r[0]:r[1]], L, iters, square, canonical),
                       idx, threads)
     return np.concatenate(parts, axis=0)
+
+
+def ecm_stage1_primes_mt(N, L, B1, sigmas, threads=None):
+    sig = np.asarray(sigmas, dtype=np.uint64)
+    threads = threads or os.cpu_count() or 1
+    count = sig.size
+    step = max(1, -(-count // (threads * 2)))
+    idx = [(s, min(count, s + step)) for s in range(0, count, step)]
+    parts = _pool_map(lambda r: ecm_stage1_primes(N, L, B1, sig[r[0]:r[1]]), idx, threads)
+    return {key: np.concatenate([p[key] for p in parts], axis=0) for key in parts[0]}
 
 
 def ecm_stage1_mt(N, L, k, sigmas, threads=None):

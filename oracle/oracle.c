@@ -432,6 +432,85 @@ static void ladder(const ctx_t *c, const uint32_t *x0m, const uint32_t *a24m, co
   *R0out = R0;
 }
 
+/* xADD with a projective difference D = (Xd:Zd) (reading G9b):
+ * U=(X0-Z0)(X1+Z1), V=(X0+Z0)(X1-Z1), X'=Zd (U+V)^2, Z'=Xd (U-V)^2 */
+static void xadd_d(const ctx_t *c, const pt_t *P0, const pt_t *P1, const pt_t *D, pt_t *out) {
+  uint32_t U[ORC_MAXL], V[ORC_MAXL], w1[ORC_MAXL], w2[ORC_MAXL];
+  msub(c, P0->X, P0->Z, w1); madd(c, P1->X, P1->Z, w2); mmul(c, w1, w2, U);
+  madd(c, P0->X, P0->Z, w1); msub(c, P1->X, P1->Z, w2); mmul(c, w1, w2, V);
+  madd(c, U, V, w1); mmul(c, w1, w1, w2); mmul(c, D->Z, w2, out->X);
+  msub(c, U, V, w1); mmul(c, w1, w1, w2); mmul(c, D->X, w2, out->Z);
+}
+
+/* Q <- [p]Q by a Montgomery ladder with difference Q: R0 = Q, R1 = xDBL(Q), then the bits of p
+ * below the top one, MSB first, as in ladder() (reading G9b). */
+static void ladder_prime(const ctx_t *c, pt_t *Q, const uint32_t *a24m, uint32_t p) {
+  pt_t D = *Q, R0 = *Q, R1, T0, T1;
+  xdbl(c, &R0, a24m, &R1);
+  int top = 31;
+  while (!((p >> top) & 1)) --top;
+  for (int i = top - 1; i >= 0; --i) {
+    if ((p >> i) & 1) {
+      xadd_d(c, &R0, &R1, &D, &T0);
+      xdbl(c, &R1, a24m, &T1);
+    } else {
+      xdbl(c, &R0, a24m, &T0);
+      xadd_d(c, &R0, &R1, &D, &T1);
+    }
+    R0 = T0;
+    R1 = T1;
+  }
+  *Q = R0;
+}
+
+int orc_ecm_stage1_primes(const uint32_t *N, int L, uint64_t B1, const uint64_t *sigmas, size_t count,
+                          uint32_t *X, uint32_t *Z, uint32_t *g, uint8_t *status, uint32_t *xaff) {
+  if (!N || L < 1 || L > ORC_MAXL || !(N[0] & 1) || B1 < 2 || B1 > 0xffffffffull) return -1;
+  /* the prime schedule: p ascending, each repeated e times with p^e <= B1 < p^(e+1) */
+  char *comp = (char *)calloc((size_t)B1 + 1, 1);
+  uint32_t *plist = (uint32_t *)malloc(sizeof(uint32_t) * ((size_t)B1 + 1));
+  if (!comp || !plist) { free(comp); free(plist); return -1; }
+  size_t np = 0;
+  for (uint64_t p = 2; p <= B1; ++p) {
+    if (comp[p]) continue;
+    for (uint64_t m = p * p; m <= B1; m += p) comp[m] = 1;
+    for (uint64_t q = p; q <= B1; q *= p) plist[np++] = (uint32_t)p;
+  }
+  free(comp);
+  ctx_t c;
+  ctx_init(&c, N, L);
+  for (size_t i = 0; i < count; ++i) {
+    uint32_t x0m[ORC_MAXL], a24m[ORC_MAXL], gg[ORC_MAXL], Xn[ORC_MAXL], Zn[ORC_MAXL], xa[ORC_MAXL];
+    zero(gg, L); gg[0] = 1;
+    zero(Xn, L); zero(Zn, L); zero(xa, L);
+    int st = suyama_mont(&c, sigmas[i], x0m, a24m, gg);
+    if (st == 0) {
+      pt_t Q;
+      copy(Q.X, x0m, L);
+      small_mont(&c, 1, Q.Z);
+      for (size_t j = 0; j < np; ++j) ladder_prime(&c, &Q, a24m, plist[j]);
+      from_mont(&c, Q.X, Xn);
+      from_mont(&c, Q.Z, Zn);
+      uint32_t zi[ORC_MAXL];
+      if (inv_gcd(Zn, c.n, L, gg, zi)) {
+        uint32_t xm[ORC_MAXL], zim[ORC_MAXL], pm[ORC_MAXL];
+        to_mont(&c, Xn, xm);
+        to_mont(&c, zi, zim);
+        mmul(&c, xm, zim, pm);
+        from_mont(&c, pm, xa);
+      }
+      st = classify(gg, N, L);
+    }
+    if (X) copy(X + i * (size_t)L, Xn, L);
+    if (Z) copy(Z + i * (size_t)L, Zn, L);
+    if (g) copy(g + i * (size_t)L, gg, L);
+    if (status) status[i] = (uint8_t)st;
+    if (xaff) copy(xaff + i * (size_t)L, xa, L);
+  }
+  free(plist);
+  return 0;
+}
+
 static int check_args(const uint32_t *N, int L, const uint32_t *k_words, uint32_t k_bits) {
   if (!N || L < 1 || L > ORC_MAXL || !(N[0] & 1) || !k_words || k_bits == 0) return -1;
   if (!bit(k_words, k_bits - 1)) return -1; /* k_bits must be exact */

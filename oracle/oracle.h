@@ -67,6 +67,14 @@ int orc_ecm_stage1(const uint32_t *N, int L, const uint32_t *k_words, uint32_t k
                    const uint64_t *sigmas, size_t count, uint32_t *X, uint32_t *Z, uint32_t *g,
                    uint8_t *status, uint32_t *xaff);
 
+/* Stage 1 with the paper-comparable schedule (reading G9b): instead of one
+ * ladder over k, Q <- [p]Q for every prime p <= B1 in ascending order, each repeated e_p times
+ * (p^e_p <= B1), each by a Montgomery ladder whose differential addition uses the projective
+ * difference Q (11 products per step).  Same outputs/conventions as orc_ecm_stage1; [k]P and so
+ * xaff and status equal orc_ecm_stage1's, X and Z differ by a projective factor. */
+int orc_ecm_stage1_primes(const uint32_t *N, int L, uint64_t B1, const uint64_t *sigmas, size_t count,
+                          uint32_t *X, uint32_t *Z, uint32_t *g, uint8_t *status, uint32_t *xaff);
+
 /* Suyama setup only (reading G10): returns status 0/3/4; on 0 writes the
  * canonical normal-domain x0 = u^3/v^3 and a24 = (v-u)^3(3u+v)/(16u^3 v). */
 int orc_suyama(const uint32_t *N, int L, uint64_t sigma, uint32_t *x0, uint32_t *a24, uint32_t *g);

@@ -18,6 +18,7 @@ ECM_CHECK = 0x8
 ECM_HOST_BUFFERS = 0x10
 ECM_NO_XAFF = 0x20
 ECM_EAGER = 0x40
+ECM_PRIME_LADDERS = 0x80
 ECM_REDC_WORD = 0 << 8
 ECM_REDC_KNOWNLOW = 1 << 8
 ECM_REDC_BLOCKTHM = 2 << 8

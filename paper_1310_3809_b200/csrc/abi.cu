@@ -26,7 +26,7 @@ namespace {
 using ecm::EcmParams;
 
 constexpr uint32_t kKnownFlags = ECM_CANONICAL | ECM_SQUARE | ECM_LAYOUT_SLICED | ECM_CHECK | ECM_HOST_BUFFERS |
-                                 ECM_NO_XAFF | ECM_EAGER | ECM_REDC_MASK;
+                                 ECM_NO_XAFF | ECM_EAGER | ECM_PRIME_LADDERS | ECM_REDC_MASK;
 
 bool valid_L(int L) { return L == 4 || L == 6 || L == 8 || L == 12; }
 
@@ -141,7 +141,25 @@ ecm_status cuda_err(cudaError_t e) {
 // ablation variants of the ECM kernel exist for L = 6 and 8 only (csrc/ecm.cu)
 bool ecm_variant_ok(int L, uint32_t flags) {
   const bool ablation = (flags & ECM_REDC_MASK) || (flags & ECM_EAGER);
+  if (flags & ECM_PRIME_LADDERS) {
+    if (L == 8) return (flags & ECM_REDC_MASK) != ECM_REDC_KNOWNLOW;
+    return L == 6 && !ablation;
+  }
   return !ablation || L == 6 || L == 8;
+}
+
+// prime schedule: p <= B1 ascending, each repeated e_p times (p^e_p <= B1), padded to 32 words
+std::vector<uint32_t> stage1_primes(uint64_t B1, uint32_t* n_out) {
+  std::vector<uint8_t> sieve(B1 + 1, 1);
+  std::vector<uint32_t> list;
+  for (uint64_t p = 2; p <= B1; ++p) {
+    if (!sieve[p]) continue;
+    for (uint64_t q = p * p; q <= B1; q += p) sieve[q] = 0;
+    for (uint64_t q = p; q <= B1; q *= p) list.push_back((uint32_t)p);
+  }
+  *n_out = (uint32_t)list.size();
+  list.resize(((list.size() + 31) / 32) * 32, 0u);
+  return list;
 }
 
 bool aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
@@ -354,13 +372,14 @@ ecm_status ecm_stage1_batch(const uint32_t* N_host, int L, uint64_t B1, const ui
   {
     PlanCache& c = cache();
     std::lock_guard<std::mutex> lock(c.mu);
-    auto it = c.plans.find({dev, B1});
+    const uint64_t key = B1 | ((flags & ECM_PRIME_LADDERS) ? (1ull << 40) : 0ull);
+    auto it = c.plans.find({dev, key});
     if (it == c.plans.end()) {
-      std::vector<uint32_t> words = stage1_scalar(B1, &kb);
+      std::vector<uint32_t> words = (flags & ECM_PRIME_LADDERS) ? stage1_primes(B1, &kb) : stage1_scalar(B1, &kb);
       e = cudaMalloc(&kw, words.size() * sizeof(uint32_t));
       if (e == cudaSuccess) e = cudaMemcpy(kw, words.data(), words.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
       if (e != cudaSuccess) return cuda_err(e);
-      c.plans[{dev, B1}] = {kw, kb};
+      c.plans[{dev, key}] = {kw, kb};
     } else {
       kw = it->second.first;
       kb = it->second.second;
@@ -377,6 +396,7 @@ ecm_status ecm_ladder_batch(const uint32_t* N_host, int L, const uint32_t* k_wor
   if (flags & (ECM_SQUARE | ECM_LAYOUT_SLICED | ECM_CANONICAL)) return ECM_E_ARG;
   if (!ecm_variant_ok(L, flags)) return ECM_E_ARG;
   if (!xaff && !(flags & ECM_NO_XAFF)) flags |= ECM_NO_XAFF;
+  if (flags & ECM_PRIME_LADDERS) return ECM_E_ARG;
   if (k_bits == 0) return ECM_E_B1;
   const size_t nw = (k_bits + 31) / 32;
   if (bitlen(k_words, (int)nw) != (int)k_bits) return ECM_E_B1;

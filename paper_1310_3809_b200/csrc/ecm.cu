@@ -213,6 +213,49 @@ __device__ __forceinline__ void ladder_step(uint32_t (&X0)[L], uint32_t (&Z0)[L]
   f.mul(Z1, x0, t4);
 }
 
+// The same step with a projective difference D = (Xd:Zd) (the paper-comparable prime-by-prime
+// schedule, reading G9b): X1' = Zd (U+V)^2, Z1' = Xd (U-V)^2 — 7M + 4S.
+template <int L, class F>
+__device__ __forceinline__ void ladder_step_d(uint32_t (&X0)[L], uint32_t (&Z0)[L], uint32_t (&X1)[L],
+                                              uint32_t (&Z1)[L], const uint32_t (&Xd)[L], const uint32_t (&Zd)[L],
+                                              const uint32_t (&a24)[L], const F& f) {
+  uint32_t t1[L], t2[L], t3[L], t4[L], U[L], V[L], s[L], d[L];
+  f.add(t1, X0, Z0);
+  f.sub(t2, X0, Z0);
+  f.add(t3, X1, Z1);
+  f.sub(t4, X1, Z1);
+  f.mul(U, t2, t3);
+  f.mul(V, t1, t4);
+  f.sqr(s, t1);
+  f.sqr(d, t2);
+  f.mul(X0, s, d);
+  f.sub(t1, s, d);
+  f.mul(t2, a24, t1);
+  f.add(t2, d, t2);
+  f.mul(Z0, t1, t2);
+  f.add(t3, U, V);
+  f.sub(t4, U, V);
+  f.sqr(t3, t3);
+  f.sqr(t4, t4);
+  f.mul(X1, Zd, t3);
+  f.mul(Z1, Xd, t4);
+}
+
+template <int L, class F>
+__device__ __forceinline__ void xdbl(uint32_t (&Xo)[L], uint32_t (&Zo)[L], const uint32_t (&X)[L], const uint32_t (&Z)[L],
+                                     const uint32_t (&a24)[L], const F& f) {
+  uint32_t t1[L], t2[L], sd[L], dd[L], tt[L];
+  f.add(t1, X, Z);
+  f.sub(t2, X, Z);
+  f.sqr(sd, t1);
+  f.sqr(dd, t2);
+  f.mul(Xo, sd, dd);
+  f.sub(tt, sd, dd);
+  f.mul(t1, a24, tt);
+  f.add(t1, dd, t1);
+  f.mul(Zo, tt, t1);
+}
+
 template <int L>
 __device__ __forceinline__ void cswap(uint32_t (&a)[L], uint32_t (&b)[L], bool c) {
 #pragma unroll
@@ -232,7 +275,7 @@ __device__ __forceinline__ void store(uint32_t* dst, size_t i, const uint32_t (&
   for (int k = 0; k < L / 2; ++k) d2[k] = make_uint2(v[2 * k], v[2 * k + 1]);
 }
 
-template <int L, int VAR, bool EAGER>
+template <int L, int VAR, bool EAGER, bool PRIMES>
 __global__ void __launch_bounds__(kEcmTPB) ecm_stage1_kernel(const __grid_constant__ EcmParams p,
                                                              const uint32_t* __restrict__ kwords, uint32_t k_bits,
                                                              const uint64_t* __restrict__ sigmas, size_t count,
@@ -318,41 +361,59 @@ __global__ void __launch_bounds__(kEcmTPB) ecm_stage1_kernel(const __grid_consta
   }
   copy(X0, x0);
   copy(Z0, ONE);
-  {
-    // R1 = xDBL(P)
-    uint32_t t1[L], t2[L], sd[L], dd[L], tt[L];
-    fld.add(t1, X0, Z0);
-    fld.sub(t2, X0, Z0);
-    fld.sqr(sd, t1);
-    fld.sqr(dd, t2);
-    fld.mul(X1, sd, dd);
-    fld.sub(tt, sd, dd);
-    fld.mul(t1, a24, tt);
-    fld.add(t1, dd, t1);
-    fld.mul(Z1, tt, t1);
-  }
-  bool swapped = false;
-  if (k_bits >= 2) {
-    int idx = (int)k_bits - 2;
-    int chunk = idx >> 10;  // 32 words = 1024 bits per warp-wide load
-    uint32_t kreg = kwords[(chunk << 5) + lane];
-    for (; idx >= 0; --idx) {
-      if ((idx >> 10) != chunk) {
-        chunk = idx >> 10;
-        kreg = kwords[(chunk << 5) + lane];
+  if (!PRIMES) xdbl<L>(X1, Z1, X0, Z0, a24, fld);  // R1 = xDBL(P)
+  if (!PRIMES) {
+    bool swapped = false;
+    if (k_bits >= 2) {
+      int idx = (int)k_bits - 2;
+      int chunk = idx >> 10;  // 32 words = 1024 bits per warp-wide load
+      uint32_t kreg = kwords[(chunk << 5) + lane];
+      for (; idx >= 0; --idx) {
+        if ((idx >> 10) != chunk) {
+          chunk = idx >> 10;
+          kreg = kwords[(chunk << 5) + lane];
+        }
+        const uint32_t word = __shfl_sync(0xffffffffu, kreg, (idx >> 5) & 31);
+        const bool bit = (word >> (idx & 31)) & 1u;
+        // bit 1: (R0, R1) <- (xADD, xDBL(R1)); bit 0: (xDBL(R0), xADD).  Double the point in the
+        // (X0,Z0) slot: swap so that slot holds R_bit, swap back lazily on the next change.
+        cswap<L>(X0, X1, bit != swapped);
+        cswap<L>(Z0, Z1, bit != swapped);
+        swapped = bit;
+        ladder_step<L>(X0, Z0, X1, Z1, x0, a24, fld);
       }
-      const uint32_t word = __shfl_sync(0xffffffffu, kreg, (idx >> 5) & 31);
-      const bool bit = (word >> (idx & 31)) & 1u;
-      // bit 1: (R0, R1) <- (xADD, xDBL(R1)); bit 0: (xDBL(R0), xADD).  Double the point in the
-      // (X0,Z0) slot: swap so that slot holds R_bit, swap back lazily on the next change.
-      cswap<L>(X0, X1, bit != swapped);
-      cswap<L>(Z0, Z1, bit != swapped);
-      swapped = bit;
-      ladder_step<L>(X0, Z0, X1, Z1, x0, a24, fld);
+    }
+    cswap<L>(X0, X1, swapped);
+    cswap<L>(Z0, Z1, swapped);
+  } else {
+    // prime-by-prime: kwords holds the list of primes p <= B1 (each repeated e_p times),
+    // k_bits its length; Q <- [p]Q by a ladder with difference Q for every entry.
+    uint32_t QX[L], QZ[L];
+    copy(QX, x0);
+    copy(QZ, ONE);
+    for (int c0 = 0; c0 < (int)k_bits; c0 += 32) {
+      const uint32_t preg = kwords[c0 + lane];
+      const int nt = ((int)k_bits - c0) < 32 ? ((int)k_bits - c0) : 32;
+      for (int t = 0; t < nt; ++t) {
+        const uint32_t pr = __shfl_sync(0xffffffffu, preg, t);
+        copy(X0, QX);
+        copy(Z0, QZ);
+        xdbl<L>(X1, Z1, QX, QZ, a24, fld);
+        bool swapped = false;
+        for (int i = 30 - __clz(pr); i >= 0; --i) {
+          const bool bit = (pr >> i) & 1u;
+          cswap<L>(X0, X1, bit != swapped);
+          cswap<L>(Z0, Z1, bit != swapped);
+          swapped = bit;
+          ladder_step_d<L>(X0, Z0, X1, Z1, QX, QZ, a24, fld);
+        }
+        cswap<L>(X0, X1, swapped);
+        cswap<L>(Z0, Z1, swapped);
+        copy(QX, X0);
+        copy(QZ, Z0);
+      }
     }
   }
-  cswap<L>(X0, X1, swapped);
-  cswap<L>(Z0, Z1, swapped);
 
   // ---------------- tail: canonical X, Z; g = gcd(Z, N); affine x ----------------
   if (!live) return;
@@ -388,12 +449,12 @@ __global__ void __launch_bounds__(kEcmTPB) ecm_stage1_kernel(const __grid_consta
   status[i] = st;
 }
 
-template <int L, int VAR, bool EAGER>
+template <int L, int VAR, bool EAGER, bool PRIMES = false>
 static cudaError_t launch_ecm_LV(const EcmParams& p, const uint32_t* kw, uint32_t k_bits, const uint64_t* sigmas,
                                  size_t count, uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status, uint32_t* xaff,
                                  uint32_t flags, cudaStream_t s) {
   const size_t blocks = (count + kEcmTPB - 1) / kEcmTPB;
-  ecm_stage1_kernel<L, VAR, EAGER><<<(unsigned)blocks, kEcmTPB, 0, s>>>(p, kw, k_bits, sigmas, count, X, Z, g,
+  ecm_stage1_kernel<L, VAR, EAGER, PRIMES><<<(unsigned)blocks, kEcmTPB, 0, s>>>(p, kw, k_bits, sigmas, count, X, Z, g,
                                                                         status, xaff, flags);
   return cudaGetLastError();
 }
@@ -406,6 +467,23 @@ static cudaError_t launch_ecm_L(const EcmParams& p, const uint32_t* kw, uint32_t
                                 uint32_t flags, cudaStream_t s) {
   const uint32_t var = (flags >> 8) & 3u;
   const bool eager = flags & 0x40u;
+  if (flags & 0x80u) {  // prime-by-prime schedule (paper-comparable)
+    if constexpr (L == 8) {
+#define ECM_PCASE(V, E) \
+      if (var == V && eager == E) return launch_ecm_LV<L, V, E, true>(p, kw, k_bits, sigmas, count, X, Z, g, status, xaff, flags, s);
+      ECM_PCASE(REDC_WORD, false)
+      ECM_PCASE(REDC_WORD, true)
+      ECM_PCASE(REDC_BLOCKTHM, false)
+      ECM_PCASE(REDC_BLOCKTHM, true)
+      ECM_PCASE(REDC_CLASSIC, false)
+      ECM_PCASE(REDC_CLASSIC, true)
+#undef ECM_PCASE
+    }
+    if constexpr (L == 6) {
+      if (var == REDC_WORD && !eager) return launch_ecm_LV<L, REDC_WORD, false, true>(p, kw, k_bits, sigmas, count, X, Z, g, status, xaff, flags, s);
+    }
+    return cudaErrorInvalidValue;
+  }
   if (var == REDC_WORD && !eager) return launch_ecm_LV<L, REDC_WORD, false>(p, kw, k_bits, sigmas, count, X, Z, g, status, xaff, flags, s);
   if constexpr (L == 6 || L == 8) {
 #define ECM_CASE(V, E) \

@@ -153,46 +153,77 @@ __device__ __forceinline__ void mont_mul_cios(uint32_t (&r)[L], const uint32_t (
 //             q1 N1, q1 N0, q0 N1 are multiplied; q0 N0 = -(T + (q1 N0 + q0 N1) h) mod R.
 // Both return the same unique raw value as mont_mul_cios.
 // ------------------------------------------------------------------------------------------
+// Schoolbook product built from the same fused IMAD.WIDE chains as the word-serial kernel:
+// each row a_i * b is split by the parity of the product offset i+j into an even-offset chain
+// (accumulator EV) and an odd-offset chain (OD); the pairs of one chain are disjoint, and with
+// rows in increasing i each chain's carry-out lands in a word that so far holds only earlier
+// carries, absorbed by one add.  t = EV + OD at the end.
 template <int A, int B>
 __device__ __forceinline__ void mul_full(uint32_t (&t)[A + B], const uint32_t* a, const uint32_t* b) {
-  // schoolbook, row by row, each row one carry chain (lo pairs then hi pairs)
+  uint32_t EV[A + B + 1], OD[A + B + 1];
 #pragma unroll
-  for (int k = 0; k < A + B; ++k) t[k] = 0;
+  for (int k = 0; k <= A + B; ++k) { EV[k] = 0; OD[k] = 0; }
 #pragma unroll
   for (int i = 0; i < A; ++i) {
-    uint32_t c = 0;
 #pragma unroll
-    for (int j = 0; j < B; ++j) {
-      // (c, t[i+j]) = a_i b_j + t[i+j] + c
-      const uint32_t lo = ptx::mad_lo_cc(a[i], b[j], t[i + j]);
-      const uint32_t hi = ptx::madc_hi(a[i], b[j], 0u);
-      t[i + j] = ptx::add_cc(lo, c);
-      c = ptx::addc(hi, 0u);
+    for (int par = 0; par < 2; ++par) {
+      uint32_t* acc = par ? OD : EV;
+      const int j0 = ((i & 1) == par) ? 0 : 1;
+      int last = -1;
+#pragma unroll
+      for (int j = j0; j < B; j += 2) {
+        const int o = i + j;
+        if (last < 0) acc[o] = ptx::mad_lo_cc(a[i], b[j], acc[o]);
+        else acc[o] = ptx::madc_lo_cc(a[i], b[j], acc[o]);
+        acc[o + 1] = ptx::madc_hi_cc(a[i], b[j], acc[o + 1]);
+        last = o;
+      }
+      if (last >= 0) acc[last + 2] = ptx::addc(acc[last + 2], 0u);
     }
-    t[i + B] = c;
   }
+  t[0] = EV[0];
+  t[1] = ptx::add_cc(EV[1], OD[1]);
+#pragma unroll
+  for (int k = 2; k < A + B - 1; ++k) t[k] = ptx::addc_cc(EV[k], OD[k]);
+  t[A + B - 1] = ptx::addc(EV[A + B - 1], OD[A + B - 1]);
 }
 
+// q = a*b mod 2^(32L): the same chains, truncated — a product at offset L-1 contributes only
+// its low word (IMAD, no high half), pairs above are not formed.
 template <int L>
 __device__ __forceinline__ void mul_low_half(uint32_t (&q)[L], const uint32_t* a, const uint32_t* b) {
-  // q = a*b mod 2^(32L)
+  uint32_t EV[L + 1], OD[L + 1];
 #pragma unroll
-  for (int k = 0; k < L; ++k) q[k] = 0;
+  for (int k = 0; k <= L; ++k) { EV[k] = 0; OD[k] = 0; }
 #pragma unroll
   for (int i = 0; i < L; ++i) {
-    uint32_t c = 0;
 #pragma unroll
-    for (int j = 0; i + j < L; ++j) {
-      if (i + j == L - 1) {
-        q[i + j] = q[i + j] + a[i] * b[j] + c;
-      } else {
-        const uint32_t lo = ptx::mad_lo_cc(a[i], b[j], q[i + j]);
-        const uint32_t hi = ptx::madc_hi(a[i], b[j], 0u);
-        q[i + j] = ptx::add_cc(lo, c);
-        c = ptx::addc(hi, 0u);
+    for (int par = 0; par < 2; ++par) {
+      uint32_t* acc = par ? OD : EV;
+      const int j0 = ((i & 1) == par) ? 0 : 1;
+      int last = -1;
+      bool closed = false;
+#pragma unroll
+      for (int j = j0; i + j < L; j += 2) {
+        const int o = i + j;
+        if (o == L - 1) {
+          acc[o] = (last < 0) ? acc[o] + a[i] * b[j] : ptx::madc_lo(a[i], b[j], acc[o]);
+          closed = true;
+        } else {
+          if (last < 0) acc[o] = ptx::mad_lo_cc(a[i], b[j], acc[o]);
+          else acc[o] = ptx::madc_lo_cc(a[i], b[j], acc[o]);
+          acc[o + 1] = ptx::madc_hi_cc(a[i], b[j], acc[o + 1]);
+        }
+        last = o;
       }
+      if (last >= 0 && !closed && last + 2 < L) acc[last + 2] = ptx::addc(acc[last + 2], 0u);
     }
   }
+  q[0] = EV[0];
+  q[1] = ptx::add_cc(EV[1], OD[1]);
+#pragma unroll
+  for (int k = 2; k < L - 1; ++k) q[k] = ptx::addc_cc(EV[k], OD[k]);
+  q[L - 1] = ptx::addc(EV[L - 1], OD[L - 1]);
 }
 
 template <int L, int V>

@@ -133,3 +133,40 @@ def test_c3_full_size_sampled(orc, torch):
     for i in flagged[:: max(1, len(flagged) // 500)]:
         g = eg.limbs_to_int(got["g"][i])
         assert 1 < g < N and N % g == 0
+
+
+@pytest.mark.parametrize("L,nbits", [(6, 190), (8, 254)])
+def test_ablation_variants_identical(orc, torch, L, nbits):
+    """Every REDC form x eager/lazy reduction ECM kernel gives the same canonical outputs (the
+    Lemma's lazy domain changes nothing observable)."""
+    cfg = ecm_config(L=L, nbits=nbits, pbits=32, B1=300, curves=70, seed=50 + L)
+    k, _ = orc.stage1_k(cfg["B1"])
+    want = orc.ecm_stage1(cfg["N"], L, k, cfg["sigmas"])
+    for var in (eg.ECM_REDC_WORD, eg.ECM_REDC_KNOWNLOW, eg.ECM_REDC_BLOCKTHM, eg.ECM_REDC_CLASSIC):
+        for eager in (0, eg.ECM_EAGER):
+            got = gpu_stage1(torch, cfg["N"], L, cfg["B1"], cfg["sigmas"], flags=var | eager)
+            assert_same(got, want)
+
+
+def test_ablation_flags_rejected_for_other_widths(torch):
+    s = torch.tensor([6, 7], dtype=torch.uint64).cuda()
+    with pytest.raises(eg.EcmError):
+        eg.ecm_stage1_batch(2 ** 120 + 1, 4, 100, s, flags=eg.ECM_EAGER)
+
+
+@pytest.mark.parametrize("L,nbits,flags", [
+    (6, 190, 0),
+    (8, 254, 0),
+    (8, 254, eg.ECM_EAGER),
+    (8, 254, eg.ECM_REDC_BLOCKTHM),
+    (8, 254, eg.ECM_REDC_CLASSIC | eg.ECM_EAGER),
+])
+def test_prime_ladder_schedule(orc, torch, L, nbits, flags):
+    """Paper-comparable prime-by-prime schedule (ECM_PRIME_LADDERS, §8(f) N2) vs the oracle's,
+    bit for bit; and the same [k]P (status, affine x) as the full-k ladder."""
+    cfg = ecm_config(L=L, nbits=nbits, pbits=32, B1=500, curves=45, seed=60 + L)
+    got = gpu_stage1(torch, cfg["N"], L, cfg["B1"], cfg["sigmas"], flags=eg.ECM_PRIME_LADDERS | flags)
+    want = orc.ecm_stage1_primes(cfg["N"], L, cfg["B1"], cfg["sigmas"])
+    assert_same(got, want)
+    full = gpu_stage1(torch, cfg["N"], L, cfg["B1"], cfg["sigmas"])
+    assert np.array_equal(full["status"], got["status"]) and np.array_equal(full["xaff"], got["xaff"])

@@ -220,3 +220,40 @@ def test_planted_prime_generator():
     assert cfg["N"] == cfg["p"] * cfg["q"]
     assert len(cfg["sigmas"]) == 1 << 20 and int(cfg["sigmas"].min()) >= 6
     assert random_prime(100, 200, 1) == random_prime(100, 200, 1)
+
+
+def test_prime_schedule_same_point(orc):
+    """The paper-comparable prime-by-prime schedule computes the same [k]P: affine x and status
+    equal the full-k ladder's (formula-free, reading G9b); X:Z differ by a projective factor."""
+    cfg = ecm_config(L=6, nbits=190, pbits=32, B1=400, curves=40, seed=9)
+    k, _ = orc.stage1_k(cfg["B1"])
+    a = orc.ecm_stage1(cfg["N"], 6, k, cfg["sigmas"])
+    b = orc.ecm_stage1_primes(cfg["N"], 6, cfg["B1"], cfg["sigmas"])
+    assert np.array_equal(a["status"], b["status"])
+    assert np.array_equal(a["xaff"], b["xaff"])
+    assert (a["status"] == 1).any()
+    ok = np.nonzero(a["status"] == 0)[0]
+    assert not np.array_equal(a["X"][ok], b["X"][ok])  # projective representatives differ
+    N = cfg["N"]
+    for i in ok[:5]:
+        X1, Z1 = orc.from_limbs(a["X"][i]), orc.from_limbs(a["Z"][i])
+        X2, Z2 = orc.from_limbs(b["X"][i]), orc.from_limbs(b["Z"][i])
+        assert (X1 * Z2 - X2 * Z1) % N == 0
+
+
+@pytest.mark.parametrize("p", [1009, 2003])
+def test_prime_schedule_small_field(orc, p):
+    """Prime-by-prime ladders over F_p agree with affine [k]P for k = lcm(1..B1)."""
+    B1 = 30
+    k, _ = orc.stage1_k(B1)
+    for sigma in (6, 7, 11):
+        c = curve_of(orc, p, sigma)
+        if c is None:
+            continue
+        A, B, x0 = c
+        r = orc.ecm_stage1_primes(p, 1, B1, [sigma])
+        Q = aff_mul(k, (x0, 1), A, B, p)
+        if Q is O:
+            assert r["status"][0] == 2
+        else:
+            assert r["status"][0] == 0 and orc.from_limbs(r["xaff"][0]) == Q[0]

@@ -29,7 +29,8 @@ def parse(path):
             toks = text.split()
             if toks and toks[0].startswith("@"):
                 toks = toks[1:]
-            funcs[cur].append((toks[0] if toks else "?", text))
+            addr = int(re.match(r"^\s+/\*([0-9a-f]+)\*/", line).group(1), 16)
+            funcs[cur].append((toks[0] if toks else "?", text, addr))
     return funcs
 
 
@@ -47,14 +48,33 @@ def main():
     ap.add_argument("--kernel", default=".")
     ap.add_argument("--min", type=int, default=1)
     ap.add_argument("--full", action="store_true", help="print the full opcode (with modifiers)")
+    ap.add_argument("--loop", action="store_true",
+                    help="count only the smallest backward-branch loop body that contains IMAD.WIDE (the hot loop)")
     a = ap.parse_args()
     funcs = parse(a.file)
     names = list(funcs)
     for raw, dem in zip(names, demangle(names)):
         if not re.search(a.kernel, dem) and not re.search(a.kernel, raw):
             continue
+        body = funcs[raw]
+        if a.loop:
+            # hot loop = the smallest backward-branch region holding >= 80% of the IMAD.WIDE/HI of
+            # the richest region (the outer grid-stride loop contains it but also the prologue)
+            regions = []
+            for k, (op, text, addr) in enumerate(body):
+                m = re.search(r"BRA(?:\.U)?\s+(?:!?U?P\w+,\s*)?0x([0-9a-f]+)", text)
+                if op.startswith("BRA") and m and int(m.group(1), 16) < addr:
+                    tgt = int(m.group(1), 16)
+                    region = [b for b in body if tgt <= b[2] <= addr]
+                    w = sum(b[0].startswith(("IMAD.WIDE", "IMAD.HI")) for b in region)
+                    regions.append((w, len(region), region))
+            if regions:
+                wmax = max(r[0] for r in regions)
+                body = min((r for r in regions if r[0] >= 0.8 * wmax), key=lambda r: r[1])[2]
+            else:
+                body = []
         c = Counter()
-        for op, _ in funcs[raw]:
+        for op, _, _ in body:
             key = op if a.full else op.split(".")[0]
             c[key] += 1
         total = sum(c.values())
