@@ -208,13 +208,29 @@ def run_ours(args):
     # ---------------- square mode and the C4 width sweep (same count, K) ----------------
     sweep = {}
     if not args.no_sweep:
-        sq = lambda: eg.ecm_mulmod_batch(A, B, Nn, out, L=L, iters=args.iters, flags=eg.ECM_SQUARE)  # noqa: E731
+        out_sq = torch.empty_like(A)
+        sq = lambda: eg.ecm_mulmod_batch(A, B, Nn, out_sq, L=L, iters=args.iters, flags=eg.ECM_SQUARE)  # noqa: E731
         sq()
         ms, _ = time_steps(torch, sq, 3, ws)
         ms = max_over_ranks(torch, ms / 3, ws)
         fpe_sq = (3 * L * L + L) // 2
+        del out_sq
         sweep["square_L6"] = {"modmul_per_s": count * args.iters * ws / (ms * 1e-3), "ms": ms,
                               "frac": count * args.iters * fpe_sq / (ms * 1e-3) / pk["fpe_peak"]}
+        # K = 1: one product per triple -> HBM bound (16L bytes per mulmod: a, b, n in, out)
+        out_k1 = torch.empty_like(A)
+        S3 = [x.reshape(count, L).t().contiguous() for x in (A, B, Nn)]
+        S_out = torch.empty_like(S3[0])
+        for tag, fn in (("k1_aos", lambda: eg.ecm_mulmod_batch(A, B, Nn, out_k1, L=L, iters=1)),
+                        ("k1_sliced", lambda: eg.ecm_mulmod_batch(S3[0], S3[1], S3[2], S_out, L=L, iters=1,
+                                                                  flags=eg.ECM_LAYOUT_SLICED))):
+            fn()
+            ms, _ = time_steps(torch, fn, 10, ws)
+            ms = max_over_ranks(torch, ms / 10, ws)
+            gbs = count * 16 * L / (ms * 1e-3) / 1e9
+            sweep[tag] = {"modmul_per_s": count * ws / (ms * 1e-3), "ms": ms, "bound": "hbm", "achieved_gbs": gbs,
+                          "peak_gbs": pk["hbm_gbs"], "frac": gbs / pk["hbm_gbs"]}
+        del out_k1, S3, S_out
         for Lw in (4, 8, 12):
             aw, bw, nw = mulmod_inputs(count, Lw, seed=4, start=rank * count)
             Aw, Bw, Nw = (torch.from_numpy(x).cuda() for x in (aw, bw, nw))
@@ -254,6 +270,7 @@ def run_ours(args):
         kb = eg.ecm_stage1_kbits(cfg["B1"])
         eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], sig[:4096], want=("g",))  # warm-up (plan, code)
         gathered = None
+        ecm_last = {}
 
         def ecm_step():
             nonlocal gathered
@@ -261,7 +278,9 @@ def run_ours(args):
                 from paper_1310_3809_b200.dist import ecm_stage1_distributed
                 gathered, _ = ecm_stage1_distributed(cfg["N"], L, cfg["B1"], cfg["sigmas"][:curves])
             else:
-                gathered = eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], sig, want=("g",))["status"]
+                r = eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], sig, want=("g",))
+                gathered = r["status"]
+                ecm_last.update(r)
 
         with ClockSampler(local) as clk2:
             ecm_ms, _ = time_steps(torch, ecm_step, 1, ws)
@@ -321,6 +340,22 @@ def run_ours(args):
     if c5:
         line["c5_shard"] = c5
     if rank == 0 and ws == 1 and not args.no_cpu:
+        # parity spot check of the timed launches against the oracle (sampled outputs)
+        import oracle
+        got = out.cpu().numpy()
+        idx = np.linspace(0, count - 1, 2048).astype(np.int64)
+        want = oracle.mulmod_chain_mt(a[idx], b[idx], n[idx], L, args.iters)
+        par = {"mulmod_checked": int(len(idx)), "mulmod_mismatches": int((got[idx] != want).any(axis=1).sum())}
+        if ecm and ecm_last:
+            cfg = ecm_config("C3")
+            k3, _ = oracle.stage1_k(cfg["B1"])
+            ci = np.linspace(0, len(ecm_last["status"]) - 1, 32).astype(np.int64)
+            w3 = oracle.ecm_stage1_mt(cfg["N"], L, k3, cfg["sigmas"][ci])
+            g3 = ecm_last["g"].cpu().numpy()[ci]
+            s3 = ecm_last["status"].cpu().numpy()[ci]
+            par["ecm_checked"] = int(len(ci))
+            par["ecm_mismatches"] = int(((g3 != w3["g"]).any(axis=1) | (s3 != w3["status"])).sum())
+        line["parity"] = par
         line["cpu_baseline"] = cpu_baseline_mulmod(args.cpu_elems, args.iters)
         if ecm:
             cfg = ecm_config("C3")

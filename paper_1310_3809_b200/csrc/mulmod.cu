@@ -6,7 +6,7 @@
 // reads its own L words (64-bit LDS, bank-conflict free for L = 6, 12).  Hot loop: `iters`
 // dependent Montgomery products entirely in registers (mont.cuh).  Stage-out mirrors stage-in.
 // The limb-sliced layout (ECM_LAYOUT_SLICED) needs no staging: limb j of the warp's 32
-// elements is one coalesced 128-byte row.
+// elements is one coalesced 128-byte row, moved with 128-bit loads through shared memory too.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -33,13 +33,58 @@ __device__ __forceinline__ void load_aos(uint32_t (&v)[L], const uint32_t* __res
   }
   __syncwarp();
   const uint2* t2 = reinterpret_cast<const uint2*>(tile) + lane * (L / 2);
+  const bool valid = lane < nvalid;  // dead lanes of a ragged tile do not read unwritten words
 #pragma unroll
   for (int k = 0; k < L / 2; ++k) {
-    const uint2 w = t2[k];
+    const uint2 w = valid ? t2[k] : make_uint2(0u, 0u);
     v[2 * k] = w.x;
     v[2 * k + 1] = w.y;
   }
   __syncwarp();
+}
+
+// Limb-sliced tile (ECM_LAYOUT_SLICED): limb j of the warp's 32 elements is the 128-byte row
+// g[j*count + e0 .. +32).  With 16-byte-aligned rows (count % 4 == 0) the warp moves the L rows
+// with 128-bit loads, 8 lanes per row, into smem tile[j*32 + lane]; each lane then reads its
+// limb j at tile[j*32 + lane] (consecutive lanes, consecutive banks: conflict-free).
+template <int L>
+__device__ __forceinline__ void load_sliced(uint32_t (&v)[L], const uint32_t* __restrict__ g, uint32_t* tile,
+                                            size_t count, size_t e0, int nvalid, int lane) {
+  if (nvalid == 32 && (count & 3) == 0) {
+    uint4* t4 = reinterpret_cast<uint4*>(tile);
+#pragma unroll
+    for (int k = lane; k < 8 * L; k += 32) {
+      const int row = k >> 3, col = k & 7;
+      t4[k] = __ldcs(reinterpret_cast<const uint4*>(g + (size_t)row * count + e0) + col);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < L; ++j) v[j] = tile[j * 32 + lane];
+    __syncwarp();
+  } else {
+#pragma unroll
+    for (int j = 0; j < L; ++j) v[j] = lane < nvalid ? __ldcs(g + (size_t)j * count + e0 + lane) : 0u;
+  }
+}
+
+template <int L>
+__device__ __forceinline__ void store_sliced(uint32_t* __restrict__ g, const uint32_t (&v)[L], uint32_t* tile,
+                                             size_t count, size_t e0, int nvalid, int lane) {
+  if (nvalid == 32 && (count & 3) == 0) {
+#pragma unroll
+    for (int j = 0; j < L; ++j) tile[j * 32 + lane] = v[j];
+    __syncwarp();
+    const uint4* t4 = reinterpret_cast<const uint4*>(tile);
+#pragma unroll
+    for (int k = lane; k < 8 * L; k += 32) {
+      const int row = k >> 3, col = k & 7;
+      __stcs(reinterpret_cast<uint4*>(g + (size_t)row * count + e0) + col, t4[k]);
+    }
+    __syncwarp();
+  } else if (lane < nvalid) {
+#pragma unroll
+    for (int j = 0; j < L; ++j) __stcs(g + (size_t)j * count + e0 + lane, v[j]);
+  }
 }
 
 template <int L>
@@ -61,7 +106,10 @@ __device__ __forceinline__ void store_aos(uint32_t* __restrict__ g, const uint32
   __syncwarp();
 }
 
-template <int L, int V, bool SQUARE>
+// P elements per thread (P = 1 or 2): with P = 2 a warp owns two 32-element tiles and every
+// thread advances two independent Montgomery chains in the same loop, giving the scheduler two
+// independent IMAD.WIDE dependency chains per warp.
+template <int L, int V, bool SQUARE, int P>
 __global__ void __launch_bounds__(kMulmodTPB) mulmod_batch_kernel(const uint32_t* __restrict__ a,
                                                                   const uint32_t* __restrict__ b,
                                                                   const uint32_t* __restrict__ n,
@@ -74,62 +122,72 @@ __global__ void __launch_bounds__(kMulmodTPB) mulmod_batch_kernel(const uint32_t
   const bool sliced = flags & 0x4u;
   const bool canon = flags & 0x1u;
   const size_t ntiles = (count + 31) / 32;
+  const size_t ngroups = (ntiles + P - 1) / P;
   const size_t warps_total = (size_t)gridDim.x * (kMulmodTPB / 32);
-  for (size_t wt = (size_t)blockIdx.x * (kMulmodTPB / 32) + warp; wt < ntiles; wt += warps_total) {
-    const size_t e0 = wt * 32;
-    const int nvalid = (int)((count - e0) < 32 ? (count - e0) : 32);
-    const size_t e = e0 + lane;
-    uint32_t x[L], y[L], nn[L];
-    if (sliced) {
-      if (lane < nvalid) {
+  for (size_t wg = (size_t)blockIdx.x * (kMulmodTPB / 32) + warp; wg < ngroups; wg += warps_total) {
+    uint32_t x[P][L], y[P][L], nn[P][L], n0inv[P];
 #pragma unroll
-        for (int k = 0; k < L; ++k) {
-          x[k] = __ldcs(a + (size_t)k * count + e);
-          nn[k] = __ldcs(n + (size_t)k * count + e);
-          y[k] = SQUARE ? 0u : __ldcs(b + (size_t)k * count + e);
-        }
+    for (int q = 0; q < P; ++q) {
+      const size_t wt = wg * P + q;
+      const size_t e0 = wt * 32;
+      const int nvalid = wt < ntiles ? (int)((count - e0) < 32 ? (count - e0) : 32) : 0;
+      if (nvalid == 0) {
+#pragma unroll
+        for (int k = 0; k < L; ++k) x[q][k] = y[q][k] = nn[q][k] = 0;
+        nn[q][0] = 1;
+      } else if (sliced) {
+        load_sliced<L>(x[q], a, tile, count, e0, nvalid, lane);
+        if (!SQUARE) load_sliced<L>(y[q], b, tile, count, e0, nvalid, lane);
+        load_sliced<L>(nn[q], n, tile, count, e0, nvalid, lane);
+        if (lane >= nvalid) nn[q][0] |= 1u;
       } else {
-#pragma unroll
-        for (int k = 0; k < L; ++k) x[k] = y[k] = nn[k] = 0;
-        nn[0] = 1;
+        load_aos<L>(x[q], a, tile, e0, nvalid, lane);
+        if (!SQUARE) load_aos<L>(y[q], b, tile, e0, nvalid, lane);
+        load_aos<L>(nn[q], n, tile, e0, nvalid, lane);
+        if (lane >= nvalid) nn[q][0] |= 1u;  // keep dead lanes' arithmetic well-defined
       }
-    } else {
-      load_aos<L>(x, a, tile, e0, nvalid, lane);
-      if (!SQUARE) load_aos<L>(y, b, tile, e0, nvalid, lane);
-      load_aos<L>(nn, n, tile, e0, nvalid, lane);
-      if (lane >= nvalid) nn[0] |= 1u;  // keep dead lanes' arithmetic well-defined
+      n0inv[q] = neg_inv32(nn[q][0]);
     }
-    const uint32_t n0inv = neg_inv32(nn[0]);
-    uint32_t np[L];
-    if (V == REDC_BLOCKTHM || V == REDC_CLASSIC) nprime_full<L>(np, nn);
-    // ---- hot loop: iters dependent lazy Montgomery products, all in registers ----
+    uint32_t np[P][L];
+    if (V == REDC_BLOCKTHM || V == REDC_CLASSIC) {
+#pragma unroll
+      for (int q = 0; q < P; ++q) nprime_full<L>(np[q], nn[q]);
+    }
+    // ---- hot loop: iters dependent lazy Montgomery products per chain, all in registers ----
 #pragma unroll 1
     for (uint32_t t = 0; t < iters; ++t) {
-      uint32_t r[L];
-      if (V == REDC_WORD || V == REDC_KNOWNLOW) {
-        if (SQUARE && V == REDC_WORD) mont_sqr<L>(r, x, nn, n0inv);
-        else if (SQUARE) mont_mul_cios<L, V>(r, x, x, nn, n0inv);
-        else mont_mul_cios<L, V>(r, x, y, nn, n0inv);
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        uint32_t r[L];
+        if (V == REDC_WORD || V == REDC_KNOWNLOW) {
+          if (SQUARE && V == REDC_WORD) mont_sqr<L>(r, x[q], nn[q], n0inv[q]);
+          else if (SQUARE) mont_mul_cios<L, V>(r, x[q], x[q], nn[q], n0inv[q]);
+          else mont_mul_cios<L, V>(r, x[q], y[q], nn[q], n0inv[q]);
+        } else {
+          if (SQUARE) mont_mul_block<L, V>(r, x[q], x[q], nn[q], np[q]);
+          else mont_mul_block<L, V>(r, x[q], y[q], nn[q], np[q]);
+        }
+#pragma unroll
+        for (int k = 0; k < L; ++k) x[q][k] = r[k];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      const size_t wt = wg * P + q;
+      if (wt >= ntiles) break;
+      const size_t e0 = wt * 32;
+      const int nvalid = (int)((count - e0) < 32 ? (count - e0) : 32);
+      if (canon) {
+        uint32_t r[L];
+        canonicalize<L>(r, x[q], nn[q]);
+#pragma unroll
+        for (int k = 0; k < L; ++k) x[q][k] = r[k];
+      }
+      if (sliced) {
+        store_sliced<L>(out, x[q], tile, count, e0, nvalid, lane);
       } else {
-        if (SQUARE) mont_mul_block<L, V>(r, x, x, nn, np);
-        else mont_mul_block<L, V>(r, x, y, nn, np);
+        store_aos<L>(out, x[q], tile, e0, nvalid, lane);
       }
-#pragma unroll
-      for (int k = 0; k < L; ++k) x[k] = r[k];
-    }
-    if (canon) {
-      uint32_t r[L];
-      canonicalize<L>(r, x, nn);
-#pragma unroll
-      for (int k = 0; k < L; ++k) x[k] = r[k];
-    }
-    if (sliced) {
-      if (lane < nvalid) {
-#pragma unroll
-        for (int k = 0; k < L; ++k) __stcs(out + (size_t)k * count + e, x[k]);
-      }
-    } else {
-      store_aos<L>(out, x, tile, e0, nvalid, lane);
     }
   }
 }
@@ -177,12 +235,14 @@ template <int L, int V>
 static cudaError_t launch_mulmod_LV(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out,
                                     size_t count, uint32_t iters, uint32_t flags, cudaStream_t s) {
   const size_t ntiles = (count + 31) / 32;
+  // P = 1: two chains per thread (P = 2) measured +0.5 % on C2 (tools/ilp_test.py) — the
+  // kernel is bound by the IMAD.WIDE pipe, not by dependency latency.
   size_t blocks = (ntiles + (kMulmodTPB / 32) - 1) / (kMulmodTPB / 32);
   if (blocks > 0x7fffffffull) blocks = 0x7fffffffull;
   if (flags & 0x2u)
-    mulmod_batch_kernel<L, V, true><<<(unsigned)blocks, kMulmodTPB, 0, s>>>(a, b, n, out, count, iters, flags);
+    mulmod_batch_kernel<L, V, true, 1><<<(unsigned)blocks, kMulmodTPB, 0, s>>>(a, b, n, out, count, iters, flags);
   else
-    mulmod_batch_kernel<L, V, false><<<(unsigned)blocks, kMulmodTPB, 0, s>>>(a, b, n, out, count, iters, flags);
+    mulmod_batch_kernel<L, V, false, 1><<<(unsigned)blocks, kMulmodTPB, 0, s>>>(a, b, n, out, count, iters, flags);
   return cudaGetLastError();
 }
 

@@ -170,3 +170,15 @@ def test_prime_ladder_schedule(orc, torch, L, nbits, flags):
     assert_same(got, want)
     full = gpu_stage1(torch, cfg["N"], L, cfg["B1"], cfg["sigmas"])
     assert np.array_equal(full["status"], got["status"]) and np.array_equal(full["xaff"], got["xaff"])
+
+
+def test_c5_sampled_curves_full_b1(orc, torch):
+    """C5's modulus and parameters (254-bit N = p*q with a planted 80-bit p, L = 8, B1 = 250000):
+    48 curves strided over the 2^22 seeds, bit-exact vs the oracle at the full B1."""
+    cfg = ecm_config("C5")
+    idx = np.arange(0, cfg["curves"], cfg["curves"] // 48)[:48] + 3
+    sig = cfg["sigmas"][idx]
+    got = gpu_stage1(torch, cfg["N"], 8, cfg["B1"], sig)
+    k, _ = orc.stage1_k(cfg["B1"])
+    want = orc.ecm_stage1_mt(cfg["N"], 8, k, sig)
+    assert_same(got, want)

@@ -1,0 +1,34 @@
+#!/usr/bin/env python3
+"""Small invocations of every launch path, for compute-sanitizer (memcheck / racecheck /
+initcheck / synccheck): AoS and sliced layouts, ragged tiles, square mode, all REDC variants,
+host-buffer staging, ECM_CHECK, every ECM width, ablation and prime-ladder variants."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1310_3809_b200 as eg  # noqa: E402
+from workload import ecm_config, mulmod_inputs  # noqa: E402
+
+torch.cuda.set_device(0)
+for L in (4, 6, 8, 12):
+    a, b, n = mulmod_inputs(32 * 3 + 5, L, seed=L, lazy=True)
+    A, B, N = (torch.from_numpy(x).cuda() for x in (a, b, n))
+    for fl in (0, eg.ECM_SQUARE, eg.ECM_CANONICAL, eg.ECM_CHECK, eg.ECM_REDC_KNOWNLOW, eg.ECM_REDC_BLOCKTHM,
+               eg.ECM_REDC_CLASSIC, eg.ECM_REDC_BLOCKTHM | eg.ECM_SQUARE):
+        eg.ecm_mulmod_batch(A, B, N, L=L, iters=2, flags=fl)
+    S = [torch.from_numpy(x.T.copy()).cuda() for x in (a, b, n)]
+    eg.ecm_mulmod_batch(*S, L=L, iters=2, flags=eg.ECM_LAYOUT_SLICED)
+    eg.ecm_mulmod_batch(a, b, n, L=L, iters=2, flags=eg.ECM_HOST_BUFFERS)
+    cfg = ecm_config(L=L, nbits=32 * L - 2, pbits=30, B1=60, curves=37, seed=L)
+    s = torch.from_numpy(cfg["sigmas"]).cuda()
+    eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], s)
+    eg.ecm_ladder_batch(cfg["N"], L, 12345, s)
+    if L in (6, 8):
+        for fl in (eg.ECM_EAGER, eg.ECM_REDC_CLASSIC, eg.ECM_PRIME_LADDERS):
+            eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], s, flags=fl, want=("g",))
+    eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], cfg["sigmas"].copy(), flags=eg.ECM_HOST_BUFFERS)
+torch.cuda.synchronize()
+print("sanitize driver done")
