@@ -105,11 +105,14 @@ def dist_env():
     return ws, rank, local
 
 
+BACKEND = os.environ.get("ECM_DIST_BACKEND", "nccl")  # gloo: exercise N > 1 on one GPU (tests only)
+
+
 def max_over_ranks(torch, x: float, ws: int) -> float:
     if ws == 1:
         return x
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if BACKEND == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -177,8 +180,8 @@ def run_ours(args):
     ws, rank, local = dist_env()
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        dist.init_process_group(BACKEND)
     else:
         torch.cuda.set_device(0)
     import paper_1310_3809_b200 as eg
@@ -231,7 +234,7 @@ def run_ours(args):
             sweep[tag] = {"modmul_per_s": count * ws / (ms * 1e-3), "ms": ms, "bound": "hbm", "achieved_gbs": gbs,
                           "peak_gbs": pk["hbm_gbs"], "frac": gbs / pk["hbm_gbs"]}
         del out_k1, S3, S_out
-        for Lw in (4, 8, 12):
+        for Lw in (4, 8, 12, 16):
             aw, bw, nw = mulmod_inputs(count, Lw, seed=4, start=rank * count)
             Aw, Bw, Nw = (torch.from_numpy(x).cuda() for x in (aw, bw, nw))
             Ow = torch.empty_like(Aw)
@@ -264,6 +267,8 @@ def run_ours(args):
     ecm = None
     if not args.no_ecm:
         cfg = ecm_config("C3")
+        if args.ecm_b1:
+            cfg["B1"] = args.ecm_b1
         curves = cfg["curves"] if args.ecm_curves is None else args.ecm_curves
         lo, hi = rank * curves // ws, (rank + 1) * curves // ws
         sig = torch.from_numpy(cfg["sigmas"][lo:hi].copy()).cuda()
@@ -276,7 +281,8 @@ def run_ours(args):
             nonlocal gathered
             if ws > 1:
                 from paper_1310_3809_b200.dist import ecm_stage1_distributed
-                gathered, _ = ecm_stage1_distributed(cfg["N"], L, cfg["B1"], cfg["sigmas"][:curves])
+                gathered, _ = ecm_stage1_distributed(cfg["N"], L, cfg["B1"], cfg["sigmas"][:curves],
+                                                     device="cuda" if BACKEND == "nccl" else "cpu")
             else:
                 r = eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], sig, want=("g",))
                 gathered = r["status"]
@@ -406,6 +412,7 @@ def main():
     ap.add_argument("--iters", type=int, default=C2_ITERS)
     ap.add_argument("--no-ecm", action="store_true")
     ap.add_argument("--ecm-curves", type=int, default=None)
+    ap.add_argument("--ecm-b1", type=int, default=None, help="override C3's B1 (tests / profiling only)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--c5", action="store_true", help="also time one rank's 1/8 shard of C5 (~40 s)")

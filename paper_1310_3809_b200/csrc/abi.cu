@@ -28,7 +28,10 @@ using ecm::EcmParams;
 constexpr uint32_t kKnownFlags = ECM_CANONICAL | ECM_SQUARE | ECM_LAYOUT_SLICED | ECM_CHECK | ECM_HOST_BUFFERS |
                                  ECM_NO_XAFF | ECM_EAGER | ECM_PRIME_LADDERS | ECM_REDC_MASK;
 
+// widths: mulmod L in {4, 6, 8, 12, 16}; ECM L in {4, 6, 8, 12} (at L = 16 the six-residue ladder
+// state does not fit the register file without splitting a curve across threads, §8(f) N3)
 bool valid_L(int L) { return L == 4 || L == 6 || L == 8 || L == 12; }
+bool valid_L_mulmod(int L) { return valid_L(L) || L == 16; }
 
 // ---- host multiprecision helpers (little-endian 32-bit words, fixed width W) ----
 int bitlen(const uint32_t* a, int W) {
@@ -299,7 +302,8 @@ uint32_t ecm_stage1_kbits(uint64_t B1) {
 ecm_status ecm_mulmod_batch(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out, size_t count,
                             int L, uint32_t iters, uint32_t flags, void* stream) {
   const bool square = flags & ECM_SQUARE;
-  if (!a || !n || !out || (!b && !square) || count == 0 || !valid_L(L) || iters == 0 || (flags & ~kKnownFlags))
+  if (!a || !n || !out || (!b && !square) || count == 0 || !valid_L_mulmod(L) || iters == 0 ||
+      (flags & ~kKnownFlags))
     return ECM_E_ARG;
   if (flags & (ECM_NO_XAFF | ECM_EAGER)) return ECM_E_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -18,6 +18,7 @@ namespace ecm {
 
 constexpr int kMulmodTPB = 256;
 
+
 // Warp-cooperative AoS tile load: words [e0*L, e0*L + nvalid*L) -> smem tile, then lane's L words.
 template <int L>
 __device__ __forceinline__ void load_aos(uint32_t (&v)[L], const uint32_t* __restrict__ g, uint32_t* tile,
@@ -106,10 +107,12 @@ __device__ __forceinline__ void store_aos(uint32_t* __restrict__ g, const uint32
   __syncwarp();
 }
 
-// P elements per thread (P = 1 or 2): with P = 2 a warp owns two 32-element tiles and every
-// thread advances two independent Montgomery chains in the same loop, giving the scheduler two
-// independent IMAD.WIDE dependency chains per warp.
-template <int L, int V, bool SQUARE, int P>
+// One thread = one element; the layout (AoS or limb-sliced) is a template parameter so that
+// each kernel carries only its own staging code (register allocation is per kernel: sharing one
+// kernel raised the AoS kernel from 40 to 56 registers and cost 3 % at C2).  Two independent
+// chains per thread were measured at +0.5 % only: the kernel is bound by the IMAD.WIDE pipe,
+// not by dependency latency.
+template <int L, int V, bool SQUARE, bool SLICED>
 __global__ void __launch_bounds__(kMulmodTPB) mulmod_batch_kernel(const uint32_t* __restrict__ a,
                                                                   const uint32_t* __restrict__ b,
                                                                   const uint32_t* __restrict__ n,
@@ -119,76 +122,49 @@ __global__ void __launch_bounds__(kMulmodTPB) mulmod_batch_kernel(const uint32_t
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   uint32_t* tile = smem + warp * 32 * L;
-  const bool sliced = flags & 0x4u;
   const bool canon = flags & 0x1u;
   const size_t ntiles = (count + 31) / 32;
-  const size_t ngroups = (ntiles + P - 1) / P;
   const size_t warps_total = (size_t)gridDim.x * (kMulmodTPB / 32);
-  for (size_t wg = (size_t)blockIdx.x * (kMulmodTPB / 32) + warp; wg < ngroups; wg += warps_total) {
-    uint32_t x[P][L], y[P][L], nn[P][L], n0inv[P];
-#pragma unroll
-    for (int q = 0; q < P; ++q) {
-      const size_t wt = wg * P + q;
-      const size_t e0 = wt * 32;
-      const int nvalid = wt < ntiles ? (int)((count - e0) < 32 ? (count - e0) : 32) : 0;
-      if (nvalid == 0) {
-#pragma unroll
-        for (int k = 0; k < L; ++k) x[q][k] = y[q][k] = nn[q][k] = 0;
-        nn[q][0] = 1;
-      } else if (sliced) {
-        load_sliced<L>(x[q], a, tile, count, e0, nvalid, lane);
-        if (!SQUARE) load_sliced<L>(y[q], b, tile, count, e0, nvalid, lane);
-        load_sliced<L>(nn[q], n, tile, count, e0, nvalid, lane);
-        if (lane >= nvalid) nn[q][0] |= 1u;
-      } else {
-        load_aos<L>(x[q], a, tile, e0, nvalid, lane);
-        if (!SQUARE) load_aos<L>(y[q], b, tile, e0, nvalid, lane);
-        load_aos<L>(nn[q], n, tile, e0, nvalid, lane);
-        if (lane >= nvalid) nn[q][0] |= 1u;  // keep dead lanes' arithmetic well-defined
-      }
-      n0inv[q] = neg_inv32(nn[q][0]);
+  for (size_t wt = (size_t)blockIdx.x * (kMulmodTPB / 32) + warp; wt < ntiles; wt += warps_total) {
+    const size_t e0 = wt * 32;
+    const int nvalid = (int)((count - e0) < 32 ? (count - e0) : 32);
+    uint32_t x[L], y[L], nn[L];
+    if (SLICED) {
+      load_sliced<L>(x, a, tile, count, e0, nvalid, lane);
+      if (!SQUARE) load_sliced<L>(y, b, tile, count, e0, nvalid, lane);
+      load_sliced<L>(nn, n, tile, count, e0, nvalid, lane);
+    } else {
+      load_aos<L>(x, a, tile, e0, nvalid, lane);
+      if (!SQUARE) load_aos<L>(y, b, tile, e0, nvalid, lane);
+      load_aos<L>(nn, n, tile, e0, nvalid, lane);
     }
-    uint32_t np[P][L];
-    if (V == REDC_BLOCKTHM || V == REDC_CLASSIC) {
-#pragma unroll
-      for (int q = 0; q < P; ++q) nprime_full<L>(np[q], nn[q]);
-    }
-    // ---- hot loop: iters dependent lazy Montgomery products per chain, all in registers ----
+    if (lane >= nvalid) nn[0] |= 1u;  // keep dead lanes' arithmetic well-defined
+    const uint32_t n0inv = neg_inv32(nn[0]);
+    uint32_t np[L];
+    if (V == REDC_BLOCKTHM || V == REDC_CLASSIC) nprime_full<L>(np, nn);
+    // ---- hot loop: iters dependent lazy Montgomery products, all in registers ----
 #pragma unroll 1
     for (uint32_t t = 0; t < iters; ++t) {
-#pragma unroll
-      for (int q = 0; q < P; ++q) {
-        uint32_t r[L];
-        if (V == REDC_WORD || V == REDC_KNOWNLOW) {
-          if (SQUARE && V == REDC_WORD) mont_sqr<L>(r, x[q], nn[q], n0inv[q]);
-          else if (SQUARE) mont_mul_cios<L, V>(r, x[q], x[q], nn[q], n0inv[q]);
-          else mont_mul_cios<L, V>(r, x[q], y[q], nn[q], n0inv[q]);
-        } else {
-          if (SQUARE) mont_mul_block<L, V>(r, x[q], x[q], nn[q], np[q]);
-          else mont_mul_block<L, V>(r, x[q], y[q], nn[q], np[q]);
-        }
-#pragma unroll
-        for (int k = 0; k < L; ++k) x[q][k] = r[k];
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < P; ++q) {
-      const size_t wt = wg * P + q;
-      if (wt >= ntiles) break;
-      const size_t e0 = wt * 32;
-      const int nvalid = (int)((count - e0) < 32 ? (count - e0) : 32);
-      if (canon) {
-        uint32_t r[L];
-        canonicalize<L>(r, x[q], nn[q]);
-#pragma unroll
-        for (int k = 0; k < L; ++k) x[q][k] = r[k];
-      }
-      if (sliced) {
-        store_sliced<L>(out, x[q], tile, count, e0, nvalid, lane);
+      uint32_t r[L];
+      if (V == REDC_WORD || V == REDC_KNOWNLOW) {
+        if (SQUARE && V == REDC_WORD) mont_sqr<L>(r, x, nn, n0inv);
+        else if (SQUARE) mont_mul_cios<L, V>(r, x, x, nn, n0inv);
+        else mont_mul_cios<L, V>(r, x, y, nn, n0inv);
       } else {
-        store_aos<L>(out, x[q], tile, e0, nvalid, lane);
+        if (SQUARE) mont_mul_block<L, V>(r, x, x, nn, np);
+        else mont_mul_block<L, V>(r, x, y, nn, np);
       }
+#pragma unroll
+      for (int k = 0; k < L; ++k) x[k] = r[k];
     }
+    if (canon) {
+      uint32_t r[L];
+      canonicalize<L>(r, x, nn);
+#pragma unroll
+      for (int k = 0; k < L; ++k) x[k] = r[k];
+    }
+    if (SLICED) store_sliced<L>(out, x, tile, count, e0, nvalid, lane);
+    else store_aos<L>(out, x, tile, e0, nvalid, lane);
   }
 }
 
@@ -235,14 +211,14 @@ template <int L, int V>
 static cudaError_t launch_mulmod_LV(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out,
                                     size_t count, uint32_t iters, uint32_t flags, cudaStream_t s) {
   const size_t ntiles = (count + 31) / 32;
-  // P = 1: two chains per thread (P = 2) measured +0.5 % on C2 (tools/ilp_test.py) — the
-  // kernel is bound by the IMAD.WIDE pipe, not by dependency latency.
   size_t blocks = (ntiles + (kMulmodTPB / 32) - 1) / (kMulmodTPB / 32);
   if (blocks > 0x7fffffffull) blocks = 0x7fffffffull;
-  if (flags & 0x2u)
-    mulmod_batch_kernel<L, V, true, 1><<<(unsigned)blocks, kMulmodTPB, 0, s>>>(a, b, n, out, count, iters, flags);
-  else
-    mulmod_batch_kernel<L, V, false, 1><<<(unsigned)blocks, kMulmodTPB, 0, s>>>(a, b, n, out, count, iters, flags);
+  const unsigned g = (unsigned)blocks;
+  const bool sq = flags & 0x2u, sl = flags & 0x4u;
+  if (sq && sl) mulmod_batch_kernel<L, V, true, true><<<g, kMulmodTPB, 0, s>>>(a, b, n, out, count, iters, flags);
+  else if (sq) mulmod_batch_kernel<L, V, true, false><<<g, kMulmodTPB, 0, s>>>(a, b, n, out, count, iters, flags);
+  else if (sl) mulmod_batch_kernel<L, V, false, true><<<g, kMulmodTPB, 0, s>>>(a, b, n, out, count, iters, flags);
+  else mulmod_batch_kernel<L, V, false, false><<<g, kMulmodTPB, 0, s>>>(a, b, n, out, count, iters, flags);
   return cudaGetLastError();
 }
 
@@ -264,6 +240,7 @@ cudaError_t launch_mulmod(const uint32_t* a, const uint32_t* b, const uint32_t* 
     case 6: return launch_mulmod_L<6>(a, b, n, out, count, iters, flags, s);
     case 8: return launch_mulmod_L<8>(a, b, n, out, count, iters, flags, s);
     case 12: return launch_mulmod_L<12>(a, b, n, out, count, iters, flags, s);
+    case 16: return launch_mulmod_L<16>(a, b, n, out, count, iters, flags, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -276,6 +253,7 @@ cudaError_t launch_mulmod_check(const uint32_t* a, const uint32_t* b, const uint
     case 6: mulmod_check_kernel<6><<<blocks, 256, 0, s>>>(a, b, n, count, flags, err); break;
     case 8: mulmod_check_kernel<8><<<blocks, 256, 0, s>>>(a, b, n, count, flags, err); break;
     case 12: mulmod_check_kernel<12><<<blocks, 256, 0, s>>>(a, b, n, count, flags, err); break;
+    case 16: mulmod_check_kernel<16><<<blocks, 256, 0, s>>>(a, b, n, count, flags, err); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -36,11 +36,17 @@ def ecm_stage1_distributed(N: int, L: int, B1: int, sigmas, *, group=None, compu
     sig = np.asarray(sigmas, dtype=np.uint64)
     count = sig.size
     lo, hi = shard_bounds(count, rank, world)
+    # the shard is computed on this rank's GPU (or wherever `compute` wants it); the gather runs
+    # on `device` (the NCCL device by default, CPU tensors under gloo)
+    compute_dev = "cuda" if (compute is None and torch.cuda.is_available()) else "cpu"
     device = device or ("cuda" if torch.cuda.is_available() else "cpu")
-    local = torch.from_numpy(sig[lo:hi].copy()).to(device)
+    local = torch.from_numpy(sig[lo:hi].copy()).to(compute_dev)
     res = (compute or _default_compute)(N, L, B1, local)
     st = res["status"].to(device)
-    g = res["g"].to(device)
+    g = res["g"]
+    if g.dtype == torch.uint32:
+        g = g.to(torch.int64)
+    g = g.to(device)
     if world == 1:
         status = st
         idx = torch.nonzero(st == 1).flatten()

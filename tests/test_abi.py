@@ -76,6 +76,10 @@ def test_argument_errors_before_any_device_work(L):
     N[5] = 0
     assert lib.ecm_stage1_batch(Np, 6, 1, sp, 4, None, None, None, stp, None, 0, None) == 4
     assert lib.ecm_stage1_batch(Np, 7, 100, sp, 4, None, None, None, stp, None, 0, None) == 1
+    N16 = np.zeros(16, np.uint32)
+    N16[0] = 11
+    assert lib.ecm_stage1_batch(N16.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), 16, 100, sp, 4,
+                                None, None, None, stp, None, 0, None) == 1  # no ECM at L = 16
     kw = np.array([5], np.uint32)
     kp = kw.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
     assert lib.ecm_ladder_batch(Np, 6, kp, 4, sp, 4, None, None, None, stp, None, 0, None) == 4  # k_bits wrong

@@ -1,0 +1,42 @@
+"""bench.py on the GPU box: the single-rank default path (shortened) and the multi-rank torchrun
+path with two ranks sharing cuda:0 (collectives over gloo; NCCL cannot put two ranks on one GPU)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+SMALL = ["--steps", "2", "--warmup", "3", "--count", "65536", "--iters", "8", "--ecm-curves", "2048",
+         "--ecm-b1", "300", "--no-sweep"]
+
+
+def _one_line(out):
+    lines = [ln for ln in out.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out
+    return json.loads(lines[0])
+
+
+def test_bench_single_rank_small():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *SMALL, "--cpu-elems", "2048",
+                        "--cpu-curves", "8"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _one_line(r.stdout)
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] == 2
+    assert d["parity"]["mulmod_mismatches"] == 0 and d["parity"]["ecm_mismatches"] == 0
+    for k in ("roofline", "cpu_baseline", "e2e", "clocks", "ecm"):
+        assert k in d
+
+
+def test_bench_two_ranks_torchrun_gloo():
+    env = dict(os.environ, ECM_DIST_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           *SMALL]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _one_line(r.stdout)
+    assert d["n_gpus"] == 2 and d["value"] > 0 and "cpu_baseline" not in d
+    assert d["ecm"]["flagged_factor"] >= 0

@@ -62,7 +62,7 @@ def lt_2n(x, n):
     return less
 
 
-@pytest.mark.parametrize("L", (4, 6, 8, 12))
+@pytest.mark.parametrize("L", (4, 6, 8, 12, 16))
 @pytest.mark.parametrize("square", (False, True))
 @pytest.mark.parametrize("layout", ("aos", "sliced"))
 def test_parity_small_all_widths(orc, torch, L, square, layout):
@@ -79,7 +79,7 @@ def test_parity_small_all_widths(orc, torch, L, square, layout):
 
 
 @pytest.mark.parametrize("variant", list(VARIANTS))
-@pytest.mark.parametrize("L", (4, 6, 8, 12))
+@pytest.mark.parametrize("L", (4, 6, 8, 12, 16))
 def test_parity_redc_variants_identical(orc, torch, variant, L):
     """Every REDC variant returns the same unique raw value."""
     count = 32 * 9 + 17
