@@ -1,12 +1,14 @@
 // mulmod.cu — batched lazy Montgomery multiplication chains (ecm_mulmod_batch), sm_100a.
 //
 // One lane = one independent (a_i, b_i, n_i) triple (north_star: "one independent modulus and
-// operand set per lane").  Stage-in: a warp moves its 32-element tile (32*L contiguous words in
-// the AoS layout) with 128-bit loads into a warp-private shared-memory tile, then each lane
-// reads its own L words (64-bit LDS, bank-conflict free for L = 6, 12).  Hot loop: `iters`
-// dependent Montgomery products entirely in registers (mont.cuh).  Stage-out mirrors stage-in.
-// The limb-sliced layout (ECM_LAYOUT_SLICED) needs no staging: limb j of the warp's 32
-// elements is one coalesced 128-byte row, moved with 128-bit loads through shared memory too.
+// operand set per lane").  Stage-in (AoS): for a full 32-element tile one lane issues bulk
+// asynchronous copies (cp.async.bulk, the TMA engine) of the a, b and n tiles — 32*L contiguous
+// words each — into warp-private shared memory, completing on a per-warp mbarrier; each lane then
+// reads its own L words.  Hot loop:
+// `iters` dependent Montgomery products entirely in registers (mont.cuh).  Stage-out: lanes write
+// their words back into the tile and one lane issues a bulk store.  Limb-sliced tiles move with
+// 128-bit loads of all three arrays in flight (load_sliced3); ragged tiles and unaligned sliced
+// rows take a 128-bit / 32-bit load path through the same tile.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -17,7 +19,45 @@
 namespace ecm {
 
 constexpr int kMulmodTPB = 256;
+// Occupancy floor for the headline kernels (AoS, word-serial REDC, L <= 6): 6 CTAs x 8 warps per
+// SM needs <= 40 registers, which the hot loop fits; other instantiations are left unconstrained.
+__host__ __device__ constexpr int mulmod_min_blocks(int L, int V, bool sliced) {
+  return (!sliced && V == 0 && L <= 6) ? 6 : 1;
+}
 
+
+// ---- bulk asynchronous copies (the TMA engine: cp.async.bulk -> SASS UBLKCP) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  } while (!done);
+}
+// global -> shared, completes on the mbarrier (size and addresses multiples of 16 bytes)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// shared -> global, tracked by bulk groups
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // Warp-cooperative AoS tile load: words [e0*L, e0*L + nvalid*L) -> smem tile, then lane's L words.
 template <int L>
@@ -68,6 +108,45 @@ __device__ __forceinline__ void load_sliced(uint32_t (&v)[L], const uint32_t* __
   }
 }
 
+// All three limb-sliced tiles at once: every lane issues its 128-bit loads of the a, b and n
+// rows before the single warp sync (3x the bytes in flight of three sequential tile loads).
+// Rows must be 16-byte aligned (count % 4 == 0) and the tile full.
+template <int L, bool SQUARE>
+__device__ __forceinline__ void load_sliced3(uint32_t (&x)[L], uint32_t (&y)[L], uint32_t (&nn)[L],
+                                             const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                                             const uint32_t* __restrict__ n, uint32_t* tA, uint32_t* tB,
+                                             uint32_t* tN, size_t count, size_t e0, int lane) {
+  constexpr int PER = (8 * L + 31) / 32;  // uint4 per lane per array
+  uint4 ra[PER], rb[PER], rn[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int k = lane + 32 * i;
+    if (k < 8 * L) {
+      const size_t off = (size_t)(k >> 3) * count + e0;
+      ra[i] = __ldcs(reinterpret_cast<const uint4*>(a + off) + (k & 7));
+      if (!SQUARE) rb[i] = __ldcs(reinterpret_cast<const uint4*>(b + off) + (k & 7));
+      rn[i] = __ldcs(reinterpret_cast<const uint4*>(n + off) + (k & 7));
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int k = lane + 32 * i;
+    if (k < 8 * L) {
+      reinterpret_cast<uint4*>(tA)[k] = ra[i];
+      if (!SQUARE) reinterpret_cast<uint4*>(tB)[k] = rb[i];
+      reinterpret_cast<uint4*>(tN)[k] = rn[i];
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    x[j] = tA[32 * j + lane];
+    y[j] = SQUARE ? 0u : tB[32 * j + lane];
+    nn[j] = tN[32 * j + lane];
+  }
+  __syncwarp();
+}
+
 template <int L>
 __device__ __forceinline__ void store_sliced(uint32_t* __restrict__ g, const uint32_t (&v)[L], uint32_t* tile,
                                              size_t count, size_t e0, int nvalid, int lane) {
@@ -113,38 +192,74 @@ __device__ __forceinline__ void store_aos(uint32_t* __restrict__ g, const uint32
 // chains per thread were measured at +0.5 % only: the kernel is bound by the IMAD.WIDE pipe,
 // not by dependency latency.
 template <int L, int V, bool SQUARE, bool SLICED>
-__global__ void __launch_bounds__(kMulmodTPB) mulmod_batch_kernel(const uint32_t* __restrict__ a,
+__global__ void __launch_bounds__(kMulmodTPB, mulmod_min_blocks(L, V, SLICED)) mulmod_batch_kernel(const uint32_t* __restrict__ a,
                                                                   const uint32_t* __restrict__ b,
                                                                   const uint32_t* __restrict__ n,
                                                                   uint32_t* out, size_t count, uint32_t iters,
                                                                   uint32_t flags) {
-  __shared__ __align__(16) uint32_t smem[kMulmodTPB * L];
+  // per warp: tiles A, B, N (32*L words each; A is reused for the output) + one mbarrier
+  extern __shared__ __align__(128) uint32_t smem[];
+  constexpr int TW = 32 * L;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  uint32_t* tile = smem + warp * 32 * L;
+  uint32_t* tA = smem + warp * 3 * TW;
+  uint32_t* tB = tA + TW;
+  uint32_t* tN = tB + TW;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (kMulmodTPB / 32) * 3 * TW) + warp;
   const bool canon = flags & 0x1u;
+  // bulk-copy path: AoS full tiles (one 32*L-word copy per array).  Limb-sliced tiles would need
+  // L 128-byte copies per array; measured slower than 128-bit loads (48.7 % vs 55.8 % of HBM at
+  // K = 1), so full aligned sliced tiles use load_sliced3 instead.
+  const bool bulk_ok = !SLICED;
+  if (lane == 0) mbar_init(bar);
+  __syncwarp();
+  uint32_t phase = 0;
   const size_t ntiles = (count + 31) / 32;
   const size_t warps_total = (size_t)gridDim.x * (kMulmodTPB / 32);
   for (size_t wt = (size_t)blockIdx.x * (kMulmodTPB / 32) + warp; wt < ntiles; wt += warps_total) {
     const size_t e0 = wt * 32;
     const int nvalid = (int)((count - e0) < 32 ? (count - e0) : 32);
     uint32_t x[L], y[L], nn[L];
-    if (SLICED) {
-      load_sliced<L>(x, a, tile, count, e0, nvalid, lane);
-      if (!SQUARE) load_sliced<L>(y, b, tile, count, e0, nvalid, lane);
-      load_sliced<L>(nn, n, tile, count, e0, nvalid, lane);
+    const bool bulk = bulk_ok && nvalid == 32;
+    if (bulk) {
+      // stage-in: one lane issues the bulk copies of all three tiles at once (TMA engine)
+      if (lane == 0) {
+        bulk_wait_read();  // the previous tile's output store has finished reading tile A
+        constexpr uint32_t bytes = 4u * TW;
+        mbar_expect_tx(bar, (SQUARE ? 2u : 3u) * bytes);
+        bulk_load(tA, a + e0 * L, bytes, bar);
+        if (!SQUARE) bulk_load(tB, b + e0 * L, bytes, bar);
+        bulk_load(tN, n + e0 * L, bytes, bar);
+      }
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+#pragma unroll
+      for (int k = 0; k < L; ++k) {
+        const int idx = lane * L + k;
+        x[k] = tA[idx];
+        y[k] = SQUARE ? 0u : tB[idx];
+        nn[k] = tN[idx];
+      }
+    } else if (SLICED && nvalid == 32 && (count & 3) == 0) {
+      load_sliced3<L, SQUARE>(x, y, nn, a, b, n, tA, tB, tN, count, e0, lane);
+    } else if (SLICED) {
+      load_sliced<L>(x, a, tA, count, e0, nvalid, lane);
+      if (!SQUARE) load_sliced<L>(y, b, tA, count, e0, nvalid, lane);
+      load_sliced<L>(nn, n, tA, count, e0, nvalid, lane);
     } else {
-      load_aos<L>(x, a, tile, e0, nvalid, lane);
-      if (!SQUARE) load_aos<L>(y, b, tile, e0, nvalid, lane);
-      load_aos<L>(nn, n, tile, e0, nvalid, lane);
+      load_aos<L>(x, a, tA, e0, nvalid, lane);
+      if (!SQUARE) load_aos<L>(y, b, tA, e0, nvalid, lane);
+      load_aos<L>(nn, n, tA, e0, nvalid, lane);
     }
     if (lane >= nvalid) nn[0] |= 1u;  // keep dead lanes' arithmetic well-defined
     const uint32_t n0inv = neg_inv32(nn[0]);
     uint32_t np[L];
     if (V == REDC_BLOCKTHM || V == REDC_CLASSIC) nprime_full<L>(np, nn);
-    // ---- hot loop: iters dependent lazy Montgomery products, all in registers ----
-#pragma unroll 1
-    for (uint32_t t = 0; t < iters; ++t) {
+    // ---- hot loop: iters dependent lazy Montgomery products, all in registers.  Unrolled by 4:
+    // ptxas then keeps the carry absorbs on the ALU pipe and renames instead of copying (SASS:
+    // 2 IMAD.X per 4 products instead of 5-7 per product; tools/loopcount.py) ----
+#pragma unroll 4
+    for (uint32_t t = iters; t != 0; --t) {
       uint32_t r[L];
       if (V == REDC_WORD || V == REDC_KNOWNLOW) {
         if (SQUARE && V == REDC_WORD) mont_sqr<L>(r, x, nn, n0inv);
@@ -163,9 +278,27 @@ __global__ void __launch_bounds__(kMulmodTPB) mulmod_batch_kernel(const uint32_t
 #pragma unroll
       for (int k = 0; k < L; ++k) x[k] = r[k];
     }
-    if (SLICED) store_sliced<L>(out, x, tile, count, e0, nvalid, lane);
-    else store_aos<L>(out, x, tile, e0, nvalid, lane);
+    if (bulk) {
+      // stage-out: each lane writes its own words of tile A (the ones it read), then one lane
+      // issues the bulk store; generic-proxy writes are fenced for the async proxy first.
+#pragma unroll
+      for (int k = 0; k < L; ++k) tA[lane * L + k] = x[k];
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        bulk_store(out + e0 * L, tA, 4u * TW);
+        bulk_commit();
+      }
+    } else if (SLICED) {
+      store_sliced<L>(out, x, tA, count, e0, nvalid, lane);
+    } else {
+      store_aos<L>(out, x, tA, e0, nvalid, lane);
+    }
+    // every lane's reads of tiles B and N precede the next bulk writes into them
+    fence_async_smem();
+    __syncwarp();
   }
+  if (lane == 0) bulk_wait_all();
 }
 
 // ---- precondition check (ECM_CHECK): n odd, bitlen(n) <= 32L-2, a, b < 2n ----
@@ -215,11 +348,20 @@ static cudaError_t launch_mulmod_LV(const uint32_t* a, const uint32_t* b, const 
   if (blocks > 0x7fffffffull) blocks = 0x7fffffffull;
   const unsigned g = (unsigned)blocks;
   const bool sq = flags & 0x2u, sl = flags & 0x4u;
-  if (sq && sl) mulmod_batch_kernel<L, V, true, true><<<g, kMulmodTPB, 0, s>>>(a, b, n, out, count, iters, flags);
-  else if (sq) mulmod_batch_kernel<L, V, true, false><<<g, kMulmodTPB, 0, s>>>(a, b, n, out, count, iters, flags);
-  else if (sl) mulmod_batch_kernel<L, V, false, true><<<g, kMulmodTPB, 0, s>>>(a, b, n, out, count, iters, flags);
-  else mulmod_batch_kernel<L, V, false, false><<<g, kMulmodTPB, 0, s>>>(a, b, n, out, count, iters, flags);
-  return cudaGetLastError();
+  constexpr size_t smem = (size_t)(kMulmodTPB / 32) * (3 * 32 * L * sizeof(uint32_t) + sizeof(uint64_t));
+  static_assert(smem <= 200 * 1024, "tile staging does not fit shared memory");
+  auto go = [&](auto kern) -> cudaError_t {
+    if (smem > 48 * 1024) {
+      const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    kern<<<g, kMulmodTPB, smem, s>>>(a, b, n, out, count, iters, flags);
+    return cudaGetLastError();
+  };
+  if (sq && sl) return go(mulmod_batch_kernel<L, V, true, true>);
+  if (sq) return go(mulmod_batch_kernel<L, V, true, false>);
+  if (sl) return go(mulmod_batch_kernel<L, V, false, true>);
+  return go(mulmod_batch_kernel<L, V, false, false>);
 }
 
 template <int L>
