@@ -302,6 +302,19 @@ def run_ours(args):
                             "frac": curves_s / ws * fpe_curve / pk["fpe_peak"]},
                "clocks": clk2.summary()}
 
+    # ---------------- C1: 256 curves, B1 = 2000 — latency bound (report time, not roofline) --------
+    c1 = None
+    if not args.no_ecm:
+        cfg1 = ecm_config("C1")
+        s1 = torch.from_numpy(cfg1["sigmas"]).cuda()
+        f1 = lambda: eg.ecm_stage1_batch(cfg1["N"], L, cfg1["B1"], s1)  # noqa: E731
+        f1()
+        ms1, _ = time_steps(torch, f1, 3, ws)
+        ms1 = max_over_ranks(torch, ms1 / 3, ws)
+        st1 = f1()["status"].cpu().numpy()
+        c1 = {"workload": "C1: 256 curves, B1=2000, 190-bit N with a planted 32-bit p (one launch)",
+              "ms": ms1, "curves": 256, "found_p": int((st1 == 1).sum())}
+
     # ---------------- optional: one rank's shard of C5 (8-GPU config) on this GPU ----------------
     c5 = None
     if args.c5:
@@ -345,6 +358,8 @@ def run_ours(args):
         line["sweep"] = sweep
     if c5:
         line["c5_shard"] = c5
+    if c1:
+        line["c1"] = c1
     if rank == 0 and ws == 1 and not args.no_cpu:
         # parity spot check of the timed launches against the oracle (sampled outputs)
         import oracle

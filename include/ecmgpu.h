@@ -65,14 +65,16 @@ typedef enum {
                                    ladders with a projective difference (11 products per step)
                                    instead of one ladder over k.  Same [k]P, status and affine x;
                                    X and Z differ by a projective factor. */
-/* REDC variant (bits 8..9): all give the SAME raw lazy value, which is a function of (T, N, R).
-   Accepted by every entry point; for ecm_stage1/ladder_batch non-default variants exist for
-   L = 6 and 8 only (ECM_E_ARG otherwise). */
+/* REDC variant (bits 8..10): all give the SAME raw lazy value, which is a function of (T, N, R).
+   ecm_mulmod_batch accepts all five; ecm_stage1/ladder_batch accept WORD for every L and
+   KNOWNLOW / BLOCKTHM / CLASSIC for L = 6 and 8 (ECM_E_ARG otherwise). */
 #define ECM_REDC_WORD (0u << 8)     /* default: word-serial CIOS, fused IMAD.WIDE carry chains */
 #define ECM_REDC_KNOWNLOW (1u << 8) /* the paper's Theorem per word: lo(m_i N_0) = -t_0 not multiplied */
 #define ECM_REDC_BLOCKTHM (2u << 8) /* block SOS with the Theorem: 3 of 4 quadrant products of q*N */
 #define ECM_REDC_CLASSIC (3u << 8)  /* block SOS, q*N as a full product (PAPER.md:93-99 as written) */
-#define ECM_REDC_MASK (3u << 8)
+#define ECM_REDC_KARATSUBA (4u << 8) /* Karatsuba products; q*N with 2 instead of 3 half-size products by
+                                        the paper's second Theorem — mulmod only */
+#define ECM_REDC_MASK (7u << 8)
 
 /* Status values written per curve by ecm_stage1_batch / ecm_ladder_batch. */
 #define ECM_CURVE_NO_FACTOR 0    /* g == 1 */

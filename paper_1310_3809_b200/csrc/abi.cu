@@ -143,6 +143,7 @@ ecm_status cuda_err(cudaError_t e) {
 
 // ablation variants of the ECM kernel exist for L = 6 and 8 only (csrc/ecm.cu)
 bool ecm_variant_ok(int L, uint32_t flags) {
+  if ((flags & ECM_REDC_MASK) > ECM_REDC_CLASSIC) return false;  // Karatsuba REDC: mulmod only
   const bool ablation = (flags & ECM_REDC_MASK) || (flags & ECM_EAGER);
   if (flags & ECM_PRIME_LADDERS) {
     if (L == 8) return (flags & ECM_REDC_MASK) != ECM_REDC_KNOWNLOW;
@@ -305,7 +306,8 @@ ecm_status ecm_mulmod_batch(const uint32_t* a, const uint32_t* b, const uint32_t
   if (!a || !n || !out || (!b && !square) || count == 0 || !valid_L_mulmod(L) || iters == 0 ||
       (flags & ~kKnownFlags))
     return ECM_E_ARG;
-  if (flags & (ECM_NO_XAFF | ECM_EAGER)) return ECM_E_ARG;
+  if (flags & (ECM_NO_XAFF | ECM_EAGER | ECM_PRIME_LADDERS)) return ECM_E_ARG;
+  if ((flags & ECM_REDC_MASK) > ECM_REDC_KARATSUBA) return ECM_E_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool host = flags & ECM_HOST_BUFFERS;
   const size_t bytes = count * (size_t)L * sizeof(uint32_t);

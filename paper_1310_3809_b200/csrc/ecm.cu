@@ -465,7 +465,7 @@ template <int L>
 static cudaError_t launch_ecm_L(const EcmParams& p, const uint32_t* kw, uint32_t k_bits, const uint64_t* sigmas,
                                 size_t count, uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status, uint32_t* xaff,
                                 uint32_t flags, cudaStream_t s) {
-  const uint32_t var = (flags >> 8) & 3u;
+  const uint32_t var = (flags >> 8) & 7u;
   const bool eager = flags & 0x40u;
   if (flags & 0x80u) {  // prime-by-prime schedule (paper-comparable)
     if constexpr (L == 8) {

@@ -26,7 +26,7 @@
 
 namespace ecm {
 
-enum RedcVariant : int { REDC_WORD = 0, REDC_KNOWNLOW = 1, REDC_BLOCKTHM = 2, REDC_CLASSIC = 3 };
+enum RedcVariant : int { REDC_WORD = 0, REDC_KNOWNLOW = 1, REDC_BLOCKTHM = 2, REDC_CLASSIC = 3, REDC_KARATSUBA = 4 };
 
 // ------------------------------------------------------------------------------------------
 // PTX carry-chain primitives.  The carry flag (CC.CF) is implicit state that links
@@ -277,6 +277,153 @@ __device__ __forceinline__ void mont_mul_block(uint32_t (&r)[L], const uint32_t 
 #pragma unroll
   for (int k = 0; k < L - 1; ++k) r[k] = ptx::addc_cc(T[L + k], QN[L + k]);
   r[L - 1] = ptx::addc(T[2 * L - 1], QN[2 * L - 1]);
+}
+
+// ------------------------------------------------------------------------------------------
+// Karatsuba-level REDC with the paper's second Theorem (Table 3: 2k-2 instead
+// of 2k-1 sub-products for k = 2).  L = 2H words, B = 2^(32H), R = B^2.
+//   T = x*y by subtractive Karatsuba: z0 = x0 y0, z2 = x1 y1, D = (x0-x1)(y1-y0) = |.||.|(+-),
+//       x0 y1 + x1 y0 = z0 + z2 + D                                   (3 H x H products)
+//   q = (T mod R) N' mod R                                           (low half)
+//   q N = w_inf B^2 + M B + w0 with w_inf = q1 N1, D2 = (q0-q1)(N1-N0), M = D2 + w0 + w_inf;
+//       w0 = q0 N0 is NOT multiplied: q N = -T (mod R) gives
+//         w0L = -T0L mod B,  w0H = ((-(T0 + w0L))/B - D2 - w0L - w_inf) mod B   (2 products)
+//   r = (T + q N)/R = T1 + w_inf + (T0 + w0 + M B)/B^2                 (exact)
+// |N1 - N0| and its sign are per-modulus constants (dN, sn), computed once per element.
+// ------------------------------------------------------------------------------------------
+// d = |a - b| over W words; returns 1 if a < b
+template <int W>
+__device__ __forceinline__ uint32_t absdiff(uint32_t (&d)[W], const uint32_t* a, const uint32_t* b) {
+  d[0] = ptx::sub_cc(a[0], b[0]);
+#pragma unroll
+  for (int k = 1; k < W; ++k) d[k] = ptx::subc_cc(a[k], b[k]);
+  const uint32_t m = ptx::subc(0u, 0u);  // all ones iff a < b
+  // conditional two's complement negate: (d ^ m) + (m & 1)
+  d[0] = ptx::add_cc(d[0] ^ m, m & 1u);
+#pragma unroll
+  for (int k = 1; k < W - 1; ++k) d[k] = ptx::addc_cc(d[k] ^ m, 0u);
+  if (W > 1) d[W - 1] = ptx::addc(d[W - 1] ^ m, 0u);
+  return m & 1u;
+}
+
+template <int L>
+__device__ __forceinline__ void kara_consts(uint32_t (&dN)[L / 2], uint32_t& sn, const uint32_t (&n)[L]) {
+  sn = absdiff<L / 2>(dN, n + L / 2, n);  // |N1 - N0|, sn = (N1 < N0)
+}
+
+template <int L>
+__device__ __forceinline__ void mont_mul_kara(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L],
+                                              const uint32_t (&n)[L], const uint32_t (&np)[L],
+                                              const uint32_t (&dN)[L / 2], uint32_t sn) {
+  constexpr int H = L / 2;
+  // ---- T = x*y ----
+  uint32_t T[2 * L];
+  {
+    uint32_t z0[2 * H], z2[2 * H], dx[H], dy[H], Dm[2 * H];
+    mul_full<H, H>(z0, x, y);
+    mul_full<H, H>(z2, x + H, y + H);
+    const uint32_t sx = absdiff<H>(dx, x, x + H);   // |x0 - x1|
+    const uint32_t sy = absdiff<H>(dy, y + H, y);   // |y1 - y0|
+    mul_full<H, H>(Dm, dx, dy);
+    const uint32_t m = 0u - (sx ^ sy);              // D = -Dm when the signs differ
+    // mid = z0 + z2 + D  (2H+1 words, >= 0)
+    uint32_t mid[2 * H + 1];
+    mid[0] = ptx::add_cc(z0[0], z2[0]);
+#pragma unroll
+    for (int k = 1; k < 2 * H; ++k) mid[k] = ptx::addc_cc(z0[k], z2[k]);
+    mid[2 * H] = ptx::addc(0u, 0u);
+    mid[0] = ptx::add_cc(mid[0], Dm[0] ^ m);
+#pragma unroll
+    for (int k = 1; k < 2 * H; ++k) mid[k] = ptx::addc_cc(mid[k], Dm[k] ^ m);
+    mid[2 * H] = ptx::addc(mid[2 * H], m);
+    mid[0] = ptx::add_cc(mid[0], m & 1u);
+#pragma unroll
+    for (int k = 1; k < 2 * H; ++k) mid[k] = ptx::addc_cc(mid[k], 0u);
+    mid[2 * H] = ptx::addc(mid[2 * H], 0u);
+    // T = z0 + z2 B^2 + mid B
+#pragma unroll
+    for (int k = 0; k < 2 * H; ++k) { T[k] = z0[k]; T[2 * H + k] = z2[k]; }
+    T[H] = ptx::add_cc(T[H], mid[0]);
+#pragma unroll
+    for (int k = 1; k <= 2 * H; ++k) T[H + k] = ptx::addc_cc(T[H + k], mid[k]);
+#pragma unroll
+    for (int k = 3 * H + 1; k < 4 * H - 1; ++k) T[k] = ptx::addc_cc(T[k], 0u);
+    if (3 * H + 1 <= 4 * H - 1) T[4 * H - 1] = ptx::addc(T[4 * H - 1], 0u);
+  }
+  // ---- q = T0 N' mod R ----
+  uint32_t q[L];
+  mul_low_half<L>(q, T, np);
+  // ---- q N with two products ----
+  uint32_t dq[H], Dm2[2 * H], winf[2 * H];
+  const uint32_t sq = absdiff<H>(dq, q, q + H);  // |q0 - q1|
+  mul_full<H, H>(Dm2, dq, dN);
+  mul_full<H, H>(winf, q + H, n + H);
+  const uint32_t m2 = 0u - (sq ^ sn);            // D2 = -Dm2 when the signs differ
+  // w0L = -T0L mod B; the low half of T0 + w0L is 0 and carries c = (T0L != 0) into word H
+  uint32_t w0[2 * H];
+  w0[0] = ptx::sub_cc(0u, T[0]);
+#pragma unroll
+  for (int k = 1; k < H; ++k) w0[k] = ptx::subc_cc(0u, T[k]);
+  const uint32_t c = ptx::subc(0u, 0u) & 1u;    // borrow iff T0L != 0
+  // U_H = -(T[H..2H) + c) mod B;  w0H = U_H - D2 - w0L - w_inf (mod B)
+  {
+    uint32_t u[H];
+    u[0] = ptx::add_cc(T[H], c);
+#pragma unroll
+    for (int k = 1; k < H; ++k) u[k] = ptx::addc_cc(T[H + k], 0u);
+    // u <- -u - w0L - winf_low  (mod B)
+    uint32_t s[H];
+    s[0] = ptx::add_cc(u[0], w0[0]);
+#pragma unroll
+    for (int k = 1; k < H; ++k) s[k] = ptx::addc_cc(u[k], w0[k]);
+    s[0] = ptx::add_cc(s[0], winf[0]);
+#pragma unroll
+    for (int k = 1; k < H; ++k) s[k] = ptx::addc_cc(s[k], winf[k]);
+    // + D2_low = +-(Dm2 low) : add (Dm2 ^ m2) + (m2 & 1)
+    s[0] = ptx::add_cc(s[0], Dm2[0] ^ m2);
+#pragma unroll
+    for (int k = 1; k < H; ++k) s[k] = ptx::addc_cc(s[k], Dm2[k] ^ m2);
+    s[0] = ptx::add_cc(s[0], m2 & 1u);
+#pragma unroll
+    for (int k = 1; k < H; ++k) s[k] = ptx::addc_cc(s[k], 0u);
+    // w0H = -s mod B
+    w0[H] = ptx::sub_cc(0u, s[0]);
+#pragma unroll
+    for (int k = 1; k < H; ++k) w0[H + k] = ptx::subc_cc(0u, s[k]);
+  }
+  // ---- M = D2 + w0 + w_inf  (2H+1 words, >= 0) ----
+  uint32_t M[2 * H + 1];
+  M[0] = ptx::add_cc(w0[0], winf[0]);
+#pragma unroll
+  for (int k = 1; k < 2 * H; ++k) M[k] = ptx::addc_cc(w0[k], winf[k]);
+  M[2 * H] = ptx::addc(0u, 0u);
+  M[0] = ptx::add_cc(M[0], Dm2[0] ^ m2);
+#pragma unroll
+  for (int k = 1; k < 2 * H; ++k) M[k] = ptx::addc_cc(M[k], Dm2[k] ^ m2);
+  M[2 * H] = ptx::addc(M[2 * H], m2);
+  M[0] = ptx::add_cc(M[0], m2 & 1u);
+#pragma unroll
+  for (int k = 1; k < 2 * H; ++k) M[k] = ptx::addc_cc(M[k], 0u);
+  M[2 * H] = ptx::addc(M[2 * H], 0u);
+  // ---- V = T0 + w0 + M B  (words 0..3H+1); only words >= 2H are needed ----
+  uint32_t V[3 * H + 2];
+  V[0] = ptx::add_cc(T[0], w0[0]);
+#pragma unroll
+  for (int k = 1; k < 2 * H; ++k) V[k] = ptx::addc_cc(T[k], w0[k]);
+  V[2 * H] = ptx::addc(0u, 0u);
+#pragma unroll
+  for (int k = 2 * H + 1; k < 3 * H + 2; ++k) V[k] = 0u;
+  V[H] = ptx::add_cc(V[H], M[0]);
+#pragma unroll
+  for (int k = 1; k <= 2 * H; ++k) V[H + k] = ptx::addc_cc(V[H + k], M[k]);
+  V[3 * H + 1] = ptx::addc(0u, 0u);
+  // ---- r = T1 + w_inf + V[2H ..] ----
+  r[0] = ptx::add_cc(T[2 * H], winf[0]);
+#pragma unroll
+  for (int k = 1; k < 2 * H; ++k) r[k] = ptx::addc_cc(T[2 * H + k], winf[k]);
+  r[0] = ptx::add_cc(r[0], V[2 * H]);
+#pragma unroll
+  for (int k = 1; k < 2 * H; ++k) r[k] = ptx::addc_cc(r[k], (k <= H + 1) ? V[2 * H + k] : 0u);
 }
 
 // ------------------------------------------------------------------------------------------

@@ -7,8 +7,8 @@
 // reads its own L words.  Hot loop:
 // `iters` dependent Montgomery products entirely in registers (mont.cuh).  Stage-out: lanes write
 // their words back into the tile and one lane issues a bulk store.  Limb-sliced tiles move with
-// 128-bit loads of all three arrays in flight (load_sliced3); ragged tiles and unaligned sliced
-// rows take a 128-bit / 32-bit load path through the same tile.
+// 128-bit loads through the tile (load_sliced); ragged tiles and unaligned sliced rows take a
+// 32-bit load path.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -108,45 +108,6 @@ __device__ __forceinline__ void load_sliced(uint32_t (&v)[L], const uint32_t* __
   }
 }
 
-// All three limb-sliced tiles at once: every lane issues its 128-bit loads of the a, b and n
-// rows before the single warp sync (3x the bytes in flight of three sequential tile loads).
-// Rows must be 16-byte aligned (count % 4 == 0) and the tile full.
-template <int L, bool SQUARE>
-__device__ __forceinline__ void load_sliced3(uint32_t (&x)[L], uint32_t (&y)[L], uint32_t (&nn)[L],
-                                             const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
-                                             const uint32_t* __restrict__ n, uint32_t* tA, uint32_t* tB,
-                                             uint32_t* tN, size_t count, size_t e0, int lane) {
-  constexpr int PER = (8 * L + 31) / 32;  // uint4 per lane per array
-  uint4 ra[PER], rb[PER], rn[PER];
-#pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    const int k = lane + 32 * i;
-    if (k < 8 * L) {
-      const size_t off = (size_t)(k >> 3) * count + e0;
-      ra[i] = __ldcs(reinterpret_cast<const uint4*>(a + off) + (k & 7));
-      if (!SQUARE) rb[i] = __ldcs(reinterpret_cast<const uint4*>(b + off) + (k & 7));
-      rn[i] = __ldcs(reinterpret_cast<const uint4*>(n + off) + (k & 7));
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    const int k = lane + 32 * i;
-    if (k < 8 * L) {
-      reinterpret_cast<uint4*>(tA)[k] = ra[i];
-      if (!SQUARE) reinterpret_cast<uint4*>(tB)[k] = rb[i];
-      reinterpret_cast<uint4*>(tN)[k] = rn[i];
-    }
-  }
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < L; ++j) {
-    x[j] = tA[32 * j + lane];
-    y[j] = SQUARE ? 0u : tB[32 * j + lane];
-    nn[j] = tN[32 * j + lane];
-  }
-  __syncwarp();
-}
-
 template <int L>
 __device__ __forceinline__ void store_sliced(uint32_t* __restrict__ g, const uint32_t (&v)[L], uint32_t* tile,
                                              size_t count, size_t e0, int nvalid, int lane) {
@@ -208,8 +169,9 @@ __global__ void __launch_bounds__(kMulmodTPB, mulmod_min_blocks(L, V, SLICED)) m
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (kMulmodTPB / 32) * 3 * TW) + warp;
   const bool canon = flags & 0x1u;
   // bulk-copy path: AoS full tiles (one 32*L-word copy per array).  Limb-sliced tiles would need
-  // L 128-byte copies per array; measured slower than 128-bit loads (48.7 % vs 55.8 % of HBM at
-  // K = 1), so full aligned sliced tiles use load_sliced3 instead.
+  // L 128-byte copies per array: measured slower than 128-bit loads (48.7 % vs 55.8 % of HBM at
+  // K = 1), and so was issuing all three arrays' 128-bit loads before one sync (51 %, 94
+  // registers), so sliced tiles use load_sliced (per array, 128-bit loads through the tile).
   const bool bulk_ok = !SLICED;
   if (lane == 0) mbar_init(bar);
   __syncwarp();
@@ -240,8 +202,6 @@ __global__ void __launch_bounds__(kMulmodTPB, mulmod_min_blocks(L, V, SLICED)) m
         y[k] = SQUARE ? 0u : tB[idx];
         nn[k] = tN[idx];
       }
-    } else if (SLICED && nvalid == 32 && (count & 3) == 0) {
-      load_sliced3<L, SQUARE>(x, y, nn, a, b, n, tA, tB, tN, count, e0, lane);
     } else if (SLICED) {
       load_sliced<L>(x, a, tA, count, e0, nvalid, lane);
       if (!SQUARE) load_sliced<L>(y, b, tA, count, e0, nvalid, lane);
@@ -253,8 +213,9 @@ __global__ void __launch_bounds__(kMulmodTPB, mulmod_min_blocks(L, V, SLICED)) m
     }
     if (lane >= nvalid) nn[0] |= 1u;  // keep dead lanes' arithmetic well-defined
     const uint32_t n0inv = neg_inv32(nn[0]);
-    uint32_t np[L];
-    if (V == REDC_BLOCKTHM || V == REDC_CLASSIC) nprime_full<L>(np, nn);
+    uint32_t np[L], dN[L / 2], sn = 0;
+    if (V == REDC_BLOCKTHM || V == REDC_CLASSIC || V == REDC_KARATSUBA) nprime_full<L>(np, nn);
+    if (V == REDC_KARATSUBA) kara_consts<L>(dN, sn, nn);
     // ---- hot loop: iters dependent lazy Montgomery products, all in registers.  Unrolled by 4:
     // ptxas then keeps the carry absorbs on the ALU pipe and renames instead of copying (SASS:
     // 2 IMAD.X per 4 products instead of 5-7 per product; tools/loopcount.py) ----
@@ -265,6 +226,9 @@ __global__ void __launch_bounds__(kMulmodTPB, mulmod_min_blocks(L, V, SLICED)) m
         if (SQUARE && V == REDC_WORD) mont_sqr<L>(r, x, nn, n0inv);
         else if (SQUARE) mont_mul_cios<L, V>(r, x, x, nn, n0inv);
         else mont_mul_cios<L, V>(r, x, y, nn, n0inv);
+      } else if (V == REDC_KARATSUBA) {
+        if (SQUARE) mont_mul_kara<L>(r, x, x, nn, np, dN, sn);
+        else mont_mul_kara<L>(r, x, y, nn, np, dN, sn);
       } else {
         if (SQUARE) mont_mul_block<L, V>(r, x, x, nn, np);
         else mont_mul_block<L, V>(r, x, y, nn, np);
@@ -367,11 +331,13 @@ static cudaError_t launch_mulmod_LV(const uint32_t* a, const uint32_t* b, const 
 template <int L>
 static cudaError_t launch_mulmod_L(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out,
                                    size_t count, uint32_t iters, uint32_t flags, cudaStream_t s) {
-  switch ((flags >> 8) & 3u) {
+  switch ((flags >> 8) & 7u) {
     case REDC_WORD: return launch_mulmod_LV<L, REDC_WORD>(a, b, n, out, count, iters, flags, s);
     case REDC_KNOWNLOW: return launch_mulmod_LV<L, REDC_KNOWNLOW>(a, b, n, out, count, iters, flags, s);
     case REDC_BLOCKTHM: return launch_mulmod_LV<L, REDC_BLOCKTHM>(a, b, n, out, count, iters, flags, s);
-    default: return launch_mulmod_LV<L, REDC_CLASSIC>(a, b, n, out, count, iters, flags, s);
+    case REDC_CLASSIC: return launch_mulmod_LV<L, REDC_CLASSIC>(a, b, n, out, count, iters, flags, s);
+    case REDC_KARATSUBA: return launch_mulmod_LV<L, REDC_KARATSUBA>(a, b, n, out, count, iters, flags, s);
+    default: return cudaErrorInvalidValue;
   }
 }
 

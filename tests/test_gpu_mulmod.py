@@ -14,7 +14,7 @@ from workload import mulmod_inputs
 pytestmark = pytest.mark.gpu
 
 VARIANTS = {"word": eg.ECM_REDC_WORD, "knownlow": eg.ECM_REDC_KNOWNLOW,
-            "blockthm": eg.ECM_REDC_BLOCKTHM, "classic": eg.ECM_REDC_CLASSIC}
+            "blockthm": eg.ECM_REDC_BLOCKTHM, "classic": eg.ECM_REDC_CLASSIC, "karatsuba": eg.ECM_REDC_KARATSUBA}
 
 
 @pytest.fixture(scope="module")

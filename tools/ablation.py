@@ -77,10 +77,24 @@ def main():
     out["paper_table5_hd5770"] = {"without_optimizations": 1.0, "section_2_2_only": 1.031,
                                   "section_2_3_only": 1.076, "fully_optimized": 1.112}
     a, b, n = (torch.from_numpy(x).cuda() for x in mulmod_inputs(1 << 24, 6, seed=2))
-    for var, name in names.items():
+    for var, name in list(names.items()) + [(eg.ECM_REDC_KARATSUBA, "karatsuba")]:
         for sq in (0, eg.ECM_SQUARE):
             ms = timed(lambda: eg.ecm_mulmod_batch(a, b, n, L=6, iters=256, flags=var | sq))
             out["mulmod"][f"{name}{'_sqr' if sq else ''}"] = {"ms": ms, "modmul_per_s": (1 << 24) * 256 / (ms * 1e-3)}
+    del a, b, n
+    # the paper's second Theorem (Karatsuba-level REDC, 2 instead of 3 half-size products for q*N,
+    # PAPER.md:262-274) against the word-serial CIOS across widths
+    out["width_karatsuba"] = {}
+    for Lw in (6, 8, 12, 16):
+        cnt = 1 << 23
+        a, b, n = (torch.from_numpy(x).cuda() for x in mulmod_inputs(cnt, Lw, seed=4))
+        row = {}
+        for var, name in ((eg.ECM_REDC_WORD, "word"), (eg.ECM_REDC_KARATSUBA, "karatsuba")):
+            for sq in (0, eg.ECM_SQUARE):
+                ms = timed(lambda: eg.ecm_mulmod_batch(a, b, n, L=Lw, iters=64, flags=var | sq))
+                row[f"{name}{'_sqr' if sq else ''}"] = cnt * 64 / (ms * 1e-3)
+        out["width_karatsuba"][f"L{Lw}"] = row
+        del a, b, n
     print(json.dumps(out))
 
 
