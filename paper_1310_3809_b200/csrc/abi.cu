@@ -197,7 +197,7 @@ ecm_status run_ecm(const uint32_t* N_host, int L, const uint32_t* kw_dev, uint32
     if (!aligned(sigmas, 8) || (X && !aligned(X, 8)) || (Z && !aligned(Z, 8)) || (g && !aligned(g, 8)) ||
         (xaff && !aligned(xaff, 8)))
       return ECM_E_ARG;
-    return cuda_err(ecm::launch_ecm(p, kw_dev, k_bits, sigmas, count, X, Z, g, status, xaff, flags, nullptr, s));
+    return cuda_err(ecm::launch_ecm(p, kw_dev, k_bits, sigmas, count, X, Z, g, status, xaff, flags, s));
   }
   // host staging: one device block for sigmas and all outputs
   const size_t res = count * L * sizeof(uint32_t);
@@ -214,7 +214,7 @@ ecm_status run_ecm(const uint32_t* N_host, int L, const uint32_t* kw_dev, uint32
   e = cudaMemcpyAsync(dsig, sigmas, count * 8, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess)
     e = ecm::launch_ecm(p, kw_dev, k_bits, dsig, count, X ? dX : nullptr, Z ? dZ : nullptr, g ? dg : nullptr, dst,
-                        xaff ? dx : nullptr, flags, nullptr, s);
+                        xaff ? dx : nullptr, flags, s);
   if (e == cudaSuccess && X) e = cudaMemcpyAsync(X, dX, res, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && Z) e = cudaMemcpyAsync(Z, dZ, res, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && g) e = cudaMemcpyAsync(g, dg, res, cudaMemcpyDeviceToHost, s);

@@ -26,9 +26,6 @@ namespace ecm {
 constexpr int kEcmTPB = 128;
 
 template <int L>
-using Res = uint32_t[L];
-
-template <int L>
 __device__ __forceinline__ const uint32_t (&cref(const uint32_t* p))[L] {
   return *reinterpret_cast<const uint32_t(*)[L]>(p);
 }
@@ -502,7 +499,7 @@ static cudaError_t launch_ecm_L(const EcmParams& p, const uint32_t* kw, uint32_t
 
 cudaError_t launch_ecm(const EcmParams& p, const uint32_t* kw, uint32_t k_bits, const uint64_t* sigmas, size_t count,
                        uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status, uint32_t* xaff, uint32_t flags,
-                       uint32_t* /*scratch*/, cudaStream_t s) {
+                       cudaStream_t s) {
   switch (p.L) {
     case 4: return launch_ecm_L<4>(p, kw, k_bits, sigmas, count, X, Z, g, status, xaff, flags, s);
     case 6: return launch_ecm_L<6>(p, kw, k_bits, sigmas, count, X, Z, g, status, xaff, flags, s);

@@ -23,6 +23,6 @@ struct EcmParams {
 
 cudaError_t launch_ecm(const EcmParams& p, const uint32_t* kbits_dev, uint32_t k_bits, const uint64_t* sigmas,
                        size_t count, uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status, uint32_t* xaff,
-                       uint32_t flags, uint32_t* scratch, cudaStream_t s);
+                       uint32_t flags, cudaStream_t s);
 
 }  // namespace ecm
