@@ -39,6 +39,31 @@ __device__ __forceinline__ void addcc(uint32_t& x, uint32_t& y, uint32_t a, uint
   asm volatile("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;" : "+r"(x), "+r"(y) : "r"(a), "r"(b));
 }
 
+__device__ __forceinline__ void dfma(double& x, double a, double b) {
+  asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(x) : "d"(a), "d"(b));
+}
+
+// FP64 FMA rate (B200 keeps a full FP64 pipe; context for DESIGN.md §9 — not used by the kernels)
+__global__ void bench_dfma(uint32_t* out, uint32_t seed, long long* cyc) {
+  double x[CHAINS];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) x[c] = 1.0 + 1e-9 * (threadIdx.x + c);
+  const double a = 0.999999 + 1e-12 * seed, b = 1e-7 * threadIdx.x;
+  __syncthreads();
+  long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int c = 0; c < CHAINS; ++c) dfma(x[c], a, b);
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) s += x[c];
+  if (s == 12345.0) out[0] = 1;
+  if (threadIdx.x == 0) atomicMax((unsigned long long*)cyc, (unsigned long long)(t1 - t0));
+}
+
 template <int MODE>
 __global__ void bench(uint32_t* out, uint32_t seed, long long* cyc) {
   uint32_t x[CHAINS], y[CHAINS], z[CHAINS];
@@ -108,5 +133,18 @@ int main() {
   run<6>("IMAD.WIDE rows + LOP3", 1, nsm, 256, 4);
   run<7>("IADD3+IADD3.X pairs", 2, nsm, 256, 4);
   run<8>("IMAD+LOP3", 1, nsm, 256, 4);
+  {
+    uint32_t* out; long long* cyc; cudaMalloc(&out, 4); cudaMalloc(&cyc, 8);
+    const int grid = nsm * 4, threads = 256;
+    bench_dfma<<<grid, threads>>>(out, 1, cyc);
+    cudaMemset(cyc, 0, 8);
+    bench_dfma<<<grid, threads>>>(out, 1, cyc);
+    cudaDeviceSynchronize();
+    long long c; cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+    const double warp_iters_smsp = (double)grid * threads / 32 * ITERS / nsm / 4;
+    const double cpi = (double)c / warp_iters_smsp;
+    printf("{\"mode\": \"DFMA (fp64 pipe)\", \"cyc_per_warp_iter_smsp\": %.3f, \"named_op_thread_per_sm_per_clk\": %.2f}\n",
+           cpi, CHAINS * 32.0 * 4 / cpi);
+  }
   return 0;
 }
