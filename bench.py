@@ -2,8 +2,9 @@
 """bench.py — throughput of the paper's hot path on B200 (arXiv 1310.3809).
 
 Default (N = 1): config C2 of BASELINE.json — 2^24 independent (a, b, N) triples of 192-bit
-(L = 6) operands, K = 256 chained lazy Montgomery products per triple; one step = one
-ecm_mulmod_batch over the whole batch (inputs resident in HBM, 1.15 GiB > L2).  Metric:
+(L = 6) operands in the limb-sliced layout, K = 256 chained lazy Montgomery products per
+triple; one step = one ecm_mulmod_batch over the whole batch (inputs resident in HBM,
+1.15 GiB > L2).  Metric:
 192-bit modmul/s.  The same JSON line carries ECM stage-1 curves/s on config C3 (B1 = 50000,
 2^20 curves, 190-bit N) measured in the same run (`ecm`), the roofline of the dominant
 kernel, the CPU oracle baseline, clocks sampled during the timed region, and the end-to-end
@@ -192,10 +193,13 @@ def run_ours(args):
     pk = peaks()
     # ---------------- C2: batched 192-bit mulmod, K = 256, this rank's replica shard ----------------
     count = args.count
+    # limb-sliced layout (north_star (1)): limb j of triple i at word [j*count + i]
     a, b, n = mulmod_inputs(count, L, seed=2, start=rank * count)
     A, B, Nn = (torch.from_numpy(x).cuda() for x in (a, b, n))
-    out = torch.empty_like(A)
-    step = lambda: eg.ecm_mulmod_batch(A, B, Nn, out, L=L, iters=args.iters)  # noqa: E731
+    S3 = [x.t().contiguous() for x in (A, B, Nn)]
+    out = torch.empty_like(S3[0])
+    step = lambda: eg.ecm_mulmod_batch(S3[0], S3[1], S3[2], out, L=L, iters=args.iters,  # noqa: E731
+                                       flags=eg.ECM_LAYOUT_SLICED)
     for _ in range(args.warmup):
         step()
     with ClockSampler(local) as clk:
@@ -211,8 +215,9 @@ def run_ours(args):
     # ---------------- square mode and the C4 width sweep (same count, K) ----------------
     sweep = {}
     if not args.no_sweep:
-        out_sq = torch.empty_like(A)
-        sq = lambda: eg.ecm_mulmod_batch(A, B, Nn, out_sq, L=L, iters=args.iters, flags=eg.ECM_SQUARE)  # noqa: E731
+        out_sq = torch.empty_like(S3[0])
+        sq = lambda: eg.ecm_mulmod_batch(S3[0], S3[1], S3[2], out_sq, L=L, iters=args.iters,  # noqa: E731
+                                         flags=eg.ECM_SQUARE | eg.ECM_LAYOUT_SLICED)
         sq()
         ms, _ = time_steps(torch, sq, 3, ws)
         ms = max_over_ranks(torch, ms / 3, ws)
@@ -221,24 +226,37 @@ def run_ours(args):
         sweep["square_L6"] = {"modmul_per_s": count * args.iters * ws / (ms * 1e-3), "ms": ms,
                               "frac": count * args.iters * fpe_sq / (ms * 1e-3) / pk["fpe_peak"]}
         # K = 1: one product per triple -> HBM bound (16L bytes per mulmod: a, b, n in, out)
+        # the AoS layout at the headline K (warp-tile kernel) for contrast
+        out_aos = torch.empty_like(A)
+        fa = lambda: eg.ecm_mulmod_batch(A, B, Nn, out_aos, L=L, iters=args.iters)  # noqa: E731
+        fa()
+        ms, _ = time_steps(torch, fa, 3, ws)
+        ms = max_over_ranks(torch, ms / 3, ws)
+        sweep["aos_L6"] = {"modmul_per_s": count * args.iters * ws / (ms * 1e-3), "ms": ms,
+                           "frac": count * args.iters * FPE_MUL / (ms * 1e-3) / pk["fpe_peak"]}
+        del out_aos
         out_k1 = torch.empty_like(A)
-        S3 = [x.reshape(count, L).t().contiguous() for x in (A, B, Nn)]
         S_out = torch.empty_like(S3[0])
-        for tag, fn in (("k1_aos", lambda: eg.ecm_mulmod_batch(A, B, Nn, out_k1, L=L, iters=1)),
-                        ("k1_sliced", lambda: eg.ecm_mulmod_batch(S3[0], S3[1], S3[2], S_out, L=L, iters=1,
-                                                                  flags=eg.ECM_LAYOUT_SLICED))):
+        # default kernel at K = 1 is the CTA-tile streaming kernel; the warp-tile kernel for contrast
+        k1 = []
+        for kname, kf in (("", 0), ("_warp", eg.ECM_KERNEL_WARP)):
+            k1.append((f"k1_aos{kname}", lambda kf=kf: eg.ecm_mulmod_batch(A, B, Nn, out_k1, L=L, iters=1, flags=kf)))
+            k1.append((f"k1_sliced{kname}", lambda kf=kf: eg.ecm_mulmod_batch(
+                S3[0], S3[1], S3[2], S_out, L=L, iters=1, flags=eg.ECM_LAYOUT_SLICED | kf)))
+        for tag, fn in k1:
             fn()
             ms, _ = time_steps(torch, fn, 10, ws)
             ms = max_over_ranks(torch, ms / 10, ws)
             gbs = count * 16 * L / (ms * 1e-3) / 1e9
             sweep[tag] = {"modmul_per_s": count * ws / (ms * 1e-3), "ms": ms, "bound": "hbm", "achieved_gbs": gbs,
                           "peak_gbs": pk["hbm_gbs"], "frac": gbs / pk["hbm_gbs"]}
-        del out_k1, S3, S_out
+        del out_k1, S_out
         for Lw in (4, 8, 12, 16):
             aw, bw, nw = mulmod_inputs(count, Lw, seed=4, start=rank * count)
-            Aw, Bw, Nw = (torch.from_numpy(x).cuda() for x in (aw, bw, nw))
+            Aw, Bw, Nw = (torch.from_numpy(x.T.copy()).cuda() for x in (aw, bw, nw))
             Ow = torch.empty_like(Aw)
-            f = lambda: eg.ecm_mulmod_batch(Aw, Bw, Nw, Ow, L=Lw, iters=args.iters)  # noqa: E731
+            f = lambda: eg.ecm_mulmod_batch(Aw, Bw, Nw, Ow, L=Lw, iters=args.iters,  # noqa: E731
+                                            flags=eg.ECM_LAYOUT_SLICED)
             f()
             ms, _ = time_steps(torch, f, 2, ws)
             ms = max_over_ranks(torch, ms / 2, ws)
@@ -248,10 +266,10 @@ def run_ours(args):
         sweep["mul_L6"] = {"bits": 190, "modmul_per_s": value, "ms": kernel_ms, "frac": achieved / pk["fpe_peak"]}
 
     # ---------------- end to end: public API with host (pinned) buffers ----------------
-    ah, bh, nh = (torch.from_numpy(x).pin_memory() for x in (a, b, n))
+    ah, bh, nh = (torch.from_numpy(x.T.copy()).pin_memory() for x in (a, b, n))
     oh = torch.empty_like(ah).pin_memory()
     e2e_step = lambda: eg.ecm_mulmod_batch(ah, bh, nh, oh, L=L, iters=args.iters,  # noqa: E731
-                                           flags=eg.ECM_HOST_BUFFERS)
+                                           flags=eg.ECM_HOST_BUFFERS | eg.ECM_LAYOUT_SLICED)
     e2e_step()
     barrier(torch, ws)
     t0 = time.perf_counter()
@@ -342,11 +360,12 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": f"C2: {count} independent (a,b,N) triples per GPU, L=6 (190-bit N), "
                                f"K={args.iters} chained lazy Montgomery products", "L": L, "count_per_gpu": count,
-                   "iters": args.iters, "redc": "word-CIOS (default)", "l2": "inputs 1.15 GiB > L2 (no flush needed)",
+                   "iters": args.iters, "redc": "word-CIOS (default)", "layout": "limb-sliced [j*count+i]",
+                   "l2": "inputs 1.15 GiB > L2 (no flush needed)",
                    "parallelism": f"replicas x{ws}"},
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": pk["fpe_peak"] / 1e12, "unit": "Tpp/s",
-                     "frac": achieved / pk["fpe_peak"], "traffic": ncu_traffic("mulmod_batch_kernel<6,0,false>"),
-                     "kernel": "ecm::mulmod_batch_kernel<6,0,false>", "kernel_ms": kernel_ms,
+                     "frac": achieved / pk["fpe_peak"], "traffic": ncu_traffic("mulmod_batch_kernel<6,0,false,true>"),
+                     "kernel": "ecm::mulmod_batch_kernel<6,0,false,true>", "kernel_ms": kernel_ms,
                      "peak_source": pk["source"],
                      "frac_at_measured_clock": (achieved / (SMS * WIDE_PER_CLK_SM * clocks["sm_mhz"] * 1e6))
                      if clocks.get("sm_mhz") else None},
@@ -363,7 +382,7 @@ def run_ours(args):
     if rank == 0 and ws == 1 and not args.no_cpu:
         # parity spot check of the timed launches against the oracle (sampled outputs)
         import oracle
-        got = out.cpu().numpy()
+        got = out.cpu().numpy().T
         idx = np.linspace(0, count - 1, 2048).astype(np.int64)
         want = oracle.mulmod_chain_mt(a[idx], b[idx], n[idx], L, args.iters)
         par = {"mulmod_checked": int(len(idx)), "mulmod_mismatches": int((got[idx] != want).any(axis=1).sum())}

@@ -75,6 +75,12 @@ typedef enum {
 #define ECM_REDC_KARATSUBA (4u << 8) /* Karatsuba products; q*N with 2 instead of 3 half-size products by
                                         the paper's second Theorem — mulmod only */
 #define ECM_REDC_MASK (7u << 8)
+/* mulmod kernel choice (diagnostic; the default picks by `iters`): the CTA-tile
+   streaming kernel (bulk-copy ring, the memory-bound regime, default for iters <= 4) or the
+   warp-tile kernel (default for longer chains).  Outputs are identical.  Sliced layouts fall
+   back to the warp-tile kernel unless count % 4 == 0 and every array is 16-byte aligned. */
+#define ECM_KERNEL_STREAM 0x800u
+#define ECM_KERNEL_WARP 0x1000u
 
 /* Status values written per curve by ecm_stage1_batch / ecm_ladder_batch. */
 #define ECM_CURVE_NO_FACTOR 0    /* g == 1 */

@@ -26,7 +26,8 @@ namespace {
 using ecm::EcmParams;
 
 constexpr uint32_t kKnownFlags = ECM_CANONICAL | ECM_SQUARE | ECM_LAYOUT_SLICED | ECM_CHECK | ECM_HOST_BUFFERS |
-                                 ECM_NO_XAFF | ECM_EAGER | ECM_PRIME_LADDERS | ECM_REDC_MASK;
+                                 ECM_NO_XAFF | ECM_EAGER | ECM_PRIME_LADDERS | ECM_REDC_MASK |
+                                 ECM_KERNEL_STREAM | ECM_KERNEL_WARP;
 
 // widths: mulmod L in {4, 6, 8, 12, 16}; ECM L in {4, 6, 8, 12} (at L = 16 the six-residue ladder
 // state does not fit the register file without splitting a curve across threads, §8(f) N3)
@@ -225,12 +226,13 @@ ecm_status run_ecm(const uint32_t* N_host, int L, const uint32_t* kw_dev, uint32
   return cuda_err(e);
 }
 
-// ECM_HOST_BUFFERS without ECM_CHECK, AoS layout: the batch is cut into chunks that cycle
+// ECM_HOST_BUFFERS without ECM_CHECK (AoS or limb-sliced): the batch is cut into chunks that cycle
 // through two internal streams, so the host->device copy of chunk c+1, the kernel of chunk c and
 // the device->host copy of chunk c-1 overlap (copy engines and SMs run concurrently).
 cudaError_t mulmod_host_pipelined(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out,
                                   size_t count, int L, uint32_t iters, uint32_t flags, cudaStream_t s) {
   const bool square = flags & ECM_SQUARE;
+  const bool sliced = flags & ECM_LAYOUT_SLICED;
   size_t chunk = (count + 7) / 8;
   if (chunk < ((size_t)1 << 18)) chunk = (size_t)1 << 18;
   chunk = (chunk + 31) / 32 * 32;
@@ -251,11 +253,26 @@ cudaError_t mulmod_host_pipelined(const uint32_t* a, const uint32_t* b, const ui
     cudaStream_t q = st[c & 1];
     uint32_t* base = scratch + (c & 1) * 4 * cw;
     uint32_t *ta = base, *tb = base + cw, *tn = base + 2 * cw, *to = base + 3 * cw;
-    e = cudaMemcpyAsync(ta, a + c0 * L, by, cudaMemcpyHostToDevice, q);
-    if (e == cudaSuccess && !square) e = cudaMemcpyAsync(tb, b + c0 * L, by, cudaMemcpyHostToDevice, q);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(tn, n + c0 * L, by, cudaMemcpyHostToDevice, q);
+    if (!sliced) {
+      e = cudaMemcpyAsync(ta, a + c0 * L, by, cudaMemcpyHostToDevice, q);
+      if (e == cudaSuccess && !square) e = cudaMemcpyAsync(tb, b + c0 * L, by, cudaMemcpyHostToDevice, q);
+      if (e == cudaSuccess) e = cudaMemcpyAsync(tn, n + c0 * L, by, cudaMemcpyHostToDevice, q);
+    } else {
+      // limb j of the chunk is the row [j*count + c0, +m) of the host array: one 2-D copy of L
+      // rows per array into a chunk-local sliced tile [j*m + i]
+      const size_t hp = count * sizeof(uint32_t), dp = m * sizeof(uint32_t);
+      e = cudaMemcpy2DAsync(ta, dp, a + c0, hp, dp, L, cudaMemcpyHostToDevice, q);
+      if (e == cudaSuccess && !square) e = cudaMemcpy2DAsync(tb, dp, b + c0, hp, dp, L, cudaMemcpyHostToDevice, q);
+      if (e == cudaSuccess) e = cudaMemcpy2DAsync(tn, dp, n + c0, hp, dp, L, cudaMemcpyHostToDevice, q);
+    }
     if (e == cudaSuccess) e = ecm::launch_mulmod(ta, square ? nullptr : tb, tn, to, m, L, iters, flags, q);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(out + c0 * L, to, by, cudaMemcpyDeviceToHost, q);
+    if (e == cudaSuccess) {
+      if (!sliced)
+        e = cudaMemcpyAsync(out + c0 * L, to, by, cudaMemcpyDeviceToHost, q);
+      else
+        e = cudaMemcpy2DAsync(out + c0, count * sizeof(uint32_t), to, m * sizeof(uint32_t), m * sizeof(uint32_t), L,
+                              cudaMemcpyDeviceToHost, q);
+    }
   }
   for (int i = 0; i < 2; ++i) {
     if (done[i] && st[i]) {
@@ -308,6 +325,7 @@ ecm_status ecm_mulmod_batch(const uint32_t* a, const uint32_t* b, const uint32_t
     return ECM_E_ARG;
   if (flags & (ECM_NO_XAFF | ECM_EAGER | ECM_PRIME_LADDERS)) return ECM_E_ARG;
   if ((flags & ECM_REDC_MASK) > ECM_REDC_KARATSUBA) return ECM_E_ARG;
+  if ((flags & ECM_KERNEL_STREAM) && (flags & ECM_KERNEL_WARP)) return ECM_E_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool host = flags & ECM_HOST_BUFFERS;
   const size_t bytes = count * (size_t)L * sizeof(uint32_t);
@@ -317,7 +335,7 @@ ecm_status ecm_mulmod_batch(const uint32_t* a, const uint32_t* b, const uint32_t
   uint32_t* dout = out;
   uint8_t* scratch = nullptr;
   cudaError_t e = cudaSuccess;
-  if (host && !(flags & (ECM_CHECK | ECM_LAYOUT_SLICED)))
+  if (host && !(flags & ECM_CHECK))
     return cuda_err(mulmod_host_pipelined(a, b, n, out, count, L, iters, flags, s));
   if (host) {
     e = dev_alloc(&scratch, 4 * bytes + 16, s);
@@ -363,7 +381,7 @@ ecm_status ecm_stage1_batch(const uint32_t* N_host, int L, uint64_t B1, const ui
                             uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status, uint32_t* xaff, uint32_t flags,
                             void* stream) {
   if (!N_host || !sigmas || !status || count == 0 || !valid_L(L) || (flags & ~kKnownFlags)) return ECM_E_ARG;
-  if (flags & (ECM_SQUARE | ECM_LAYOUT_SLICED | ECM_CANONICAL)) return ECM_E_ARG;
+  if (flags & (ECM_SQUARE | ECM_LAYOUT_SLICED | ECM_CANONICAL | ECM_KERNEL_STREAM | ECM_KERNEL_WARP)) return ECM_E_ARG;
   if (!ecm_variant_ok(L, flags)) return ECM_E_ARG;
   if (!xaff && !(flags & ECM_NO_XAFF)) flags |= ECM_NO_XAFF;
   if (B1 < 2 || B1 >= (1ull << 32)) return ECM_E_B1;
@@ -399,7 +417,7 @@ ecm_status ecm_ladder_batch(const uint32_t* N_host, int L, const uint32_t* k_wor
                             uint8_t* status, uint32_t* xaff, uint32_t flags, void* stream) {
   if (!N_host || !k_words || !sigmas || !status || count == 0 || !valid_L(L) || (flags & ~kKnownFlags))
     return ECM_E_ARG;
-  if (flags & (ECM_SQUARE | ECM_LAYOUT_SLICED | ECM_CANONICAL)) return ECM_E_ARG;
+  if (flags & (ECM_SQUARE | ECM_LAYOUT_SLICED | ECM_CANONICAL | ECM_KERNEL_STREAM | ECM_KERNEL_WARP)) return ECM_E_ARG;
   if (!ecm_variant_ok(L, flags)) return ECM_E_ARG;
   if (!xaff && !(flags & ECM_NO_XAFF)) flags |= ECM_NO_XAFF;
   if (flags & ECM_PRIME_LADDERS) return ECM_E_ARG;

@@ -1,501 +1,17 @@
-// ecm.cu — ECM stage 1, one curve per thread, sm_100a.
-//
-// Per thread (one curve, no inter-thread synchronisation: PAPER.md:312):
-//   setup  : Brent-Suyama curve from sigma (formulas: DESIGN.md reading G10)
-//            u = s^2-5, v = 4s, D = 16u^3v^4, one inversion w = D^{-1} (per-thread binary
-//            extended gcd), x0 = 16u^6 v w, a24 = (v-u)^3(3u+v) v^3 w.  gcd(D, N) != 1 ->
-//            status 3 / 4 (the setup denominator "is not invertible").
-//   ladder : R0 = (x0:1), R1 = xDBL(R0); for each further bit of k (MSB first) one combined
-//            xADD + xDBL step, 6M + 4S + 8 lazy add/sub.  k is shared by every
-//            curve, so the bit is warp-uniform: the conditional swap is a uniform select and
-//            the k words are broadcast across the warp with __shfl_sync.
-//   tail   : X, Z out of Montgomery form, canonical; g = gcd(Z, N) by the same binary extended
-//            gcd, which also yields Z^{-1} for the affine x = X/Z ("its gcd gives a factor of n",
-//            PAPER.md:302).
-// N, 2N, R^2 mod N, R mod N and -N^{-1} mod 2^32 are shared by all curves and live in the kernel
-// parameter (constant) bank, so the hot loop reads N directly as IMAD constant operands.
+// ecm.cu — dispatch of the ECM stage-1 kernels by width.  The kernels are in ecm_kernels.cuh,
+// instantiated per width in ecm_l<L>.cu.
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
 #include "kernels.h"
-#include "mont.cuh"
 
 namespace ecm {
 
-constexpr int kEcmTPB = 128;
-
 template <int L>
-__device__ __forceinline__ const uint32_t (&cref(const uint32_t* p))[L] {
-  return *reinterpret_cast<const uint32_t(*)[L]>(p);
-}
-
-template <int L>
-__device__ __forceinline__ void copy(uint32_t (&d)[L], const uint32_t (&s)[L]) {
-#pragma unroll
-  for (int k = 0; k < L; ++k) d[k] = s[k];
-}
-
-template <int L>
-__device__ __forceinline__ bool is_zero(const uint32_t (&a)[L]) {
-  uint32_t o = 0;
-#pragma unroll
-  for (int k = 0; k < L; ++k) o |= a[k];
-  return o == 0;
-}
-
-template <int L>
-__device__ __forceinline__ bool is_one(const uint32_t (&a)[L]) {
-  uint32_t o = a[0] ^ 1u;
-#pragma unroll
-  for (int k = 1; k < L; ++k) o |= a[k];
-  return o == 0;
-}
-
-template <int L>
-__device__ __forceinline__ bool equal(const uint32_t (&a)[L], const uint32_t (&b)[L]) {
-  uint32_t o = 0;
-#pragma unroll
-  for (int k = 0; k < L; ++k) o |= a[k] ^ b[k];
-  return o == 0;
-}
-
-// a >= b ?
-template <int L>
-__device__ __forceinline__ bool geq(const uint32_t (&a)[L], const uint32_t (&b)[L]) {
-  (void)ptx::sub_cc(a[0], b[0]);
-#pragma unroll
-  for (int k = 1; k < L; ++k) (void)ptx::subc_cc(a[k], b[k]);
-  return ptx::subc(0u, 0u) == 0u;
-}
-
-template <int L>
-__device__ __forceinline__ void sub_plain(uint32_t (&d)[L], const uint32_t (&a)[L], const uint32_t (&b)[L]) {
-  d[0] = ptx::sub_cc(a[0], b[0]);
-#pragma unroll
-  for (int k = 1; k < L - 1; ++k) d[k] = ptx::subc_cc(a[k], b[k]);
-  d[L - 1] = ptx::subc(a[L - 1], b[L - 1]);
-}
-
-// x = x/2 mod N for x < N (N odd): add N when x is odd, then shift the (L*32+1)-bit sum.
-template <int L>
-__device__ __forceinline__ void half_mod(uint32_t (&x)[L], const uint32_t (&N)[L]) {
-  const uint32_t mask = 0u - (x[0] & 1u);
-  uint32_t s[L];
-  s[0] = ptx::add_cc(x[0], N[0] & mask);
-#pragma unroll
-  for (int k = 1; k < L; ++k) s[k] = ptx::addc_cc(x[k], N[k] & mask);
-  const uint32_t top = ptx::addc(0u, 0u);
-#pragma unroll
-  for (int k = 0; k < L - 1; ++k) x[k] = __funnelshift_r(s[k], s[k + 1], 1);
-  x[L - 1] = __funnelshift_r(s[L - 1], top, 1);
-}
-
-template <int L>
-__device__ __forceinline__ void shr1(uint32_t (&x)[L]) {
-#pragma unroll
-  for (int k = 0; k < L - 1; ++k) x[k] = __funnelshift_r(x[k], x[k + 1], 1);
-  x[L - 1] >>= 1;
-}
-
-// d = a - b mod N for a, b < N
-template <int L>
-__device__ __forceinline__ void sub_modN(uint32_t (&d)[L], const uint32_t (&a)[L], const uint32_t (&b)[L],
-                                         const uint32_t (&N)[L]) {
-  uint32_t t[L];
-  t[0] = ptx::sub_cc(a[0], b[0]);
-#pragma unroll
-  for (int k = 1; k < L; ++k) t[k] = ptx::subc_cc(a[k], b[k]);
-  const uint32_t mask = ptx::subc(0u, 0u);
-  d[0] = ptx::add_cc(t[0], N[0] & mask);
-#pragma unroll
-  for (int k = 1; k < L - 1; ++k) d[k] = ptx::addc_cc(t[k], N[k] & mask);
-  d[L - 1] = ptx::addc(t[L - 1], N[L - 1] & mask);
-}
-
-// Binary extended gcd ("right-shift" form, v kept odd):
-//   u = a, v = N, A = 1, C = 0 with A a = u, C a = v (mod N);
-//   while u != 0: strip factors 2 from u (halving A mod N); if u < v swap (u,A) <-> (v,C);
-//   u -= v, A -= C.   On exit v = gcd(a, N) and, if v == 1, C = a^{-1} mod N.
-// a < N canonical, N odd.  Returns true iff invertible.  Data-dependent trip count (setup and
-// tail only: < 0.5% of a curve at the smallest B1).
-template <int L>
-__device__ bool xgcd(const uint32_t (&a)[L], const uint32_t (&N)[L], uint32_t (&g)[L], uint32_t (&inv)[L]) {
-  uint32_t u[L], v[L], A[L], C[L];
-  copy(u, a);
-  copy(v, N);
-#pragma unroll
-  for (int k = 0; k < L; ++k) { A[k] = 0; C[k] = 0; }
-  A[0] = 1;
-  while (!is_zero(u)) {
-    while (!(u[0] & 1u)) {
-      shr1(u);
-      half_mod(A, N);
-    }
-    if (!geq(u, v)) {
-#pragma unroll
-      for (int k = 0; k < L; ++k) {
-        uint32_t t = u[k]; u[k] = v[k]; v[k] = t;
-        t = A[k]; A[k] = C[k]; C[k] = t;
-      }
-    }
-    sub_plain(u, u, v);
-    sub_modN(A, A, C, N);
-  }
-  copy(g, v);
-  copy(inv, C);
-  return is_one(v);
-}
-
-// ---------------------------------------------------------------------------------------
-// Field products of the ladder, templated for the paper's ablation (Table 5 analogue, §8(f) N1):
-//   V     : REDC variant (mont.cuh); all give the same raw value.
-//   EAGER : canonicalise after every product and reduce add/sub modulo N (the "without
-//           Section 2.2" baseline: 18 conditional reductions per step instead of 8).
-// ---------------------------------------------------------------------------------------
-template <int L, int V, bool EAGER>
-struct Field {
-  const uint32_t (&N)[L];
-  const uint32_t (&M)[L];   // add/sub modulus: 2N (lazy) or N (eager)
-  const uint32_t (&NP)[L];  // -N^{-1} mod R (block variants)
-  uint32_t n0inv;
-  __device__ __forceinline__ void mul(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L]) const {
-    if (V == REDC_WORD || V == REDC_KNOWNLOW) mont_mul_cios<L, V>(r, x, y, N, n0inv);
-    else mont_mul_block<L, V>(r, x, y, N, NP);
-    if (EAGER) canonicalize<L>(r, r, N);
-  }
-  __device__ __forceinline__ void sqr(uint32_t (&r)[L], const uint32_t (&x)[L]) const {
-    if (V == REDC_WORD) mont_sqr<L>(r, x, N, n0inv);
-    else if (V == REDC_KNOWNLOW) mont_mul_cios<L, V>(r, x, x, N, n0inv);
-    else mont_mul_block<L, V>(r, x, x, N, NP);
-    if (EAGER) canonicalize<L>(r, r, N);
-  }
-  __device__ __forceinline__ void add(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L]) const {
-    add_lazy<L>(r, x, y, M);
-  }
-  __device__ __forceinline__ void sub(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L]) const {
-    sub_lazy<L>(r, x, y, M);
-  }
-};
-
-// ---------------------------------------------------------------------------------------
-// One combined ladder step on (X0:Z0) [doubled] and (X1:Z1) [added], difference (x0:1):
-//   t1 = X0+Z0, t2 = X0-Z0, t3 = X1+Z1, t4 = X1-Z1
-//   U = t2 t3, V = t1 t4, s = t1^2, d = t2^2
-//   X0' = s d,  t = s - d,  Z0' = t (d + a24 t)
-//   X1' = (U+V)^2,  Z1' = x0 (U-V)^2
-// ---------------------------------------------------------------------------------------
-template <int L, class F>
-__device__ __forceinline__ void ladder_step(uint32_t (&X0)[L], uint32_t (&Z0)[L], uint32_t (&X1)[L],
-                                            uint32_t (&Z1)[L], const uint32_t (&x0)[L], const uint32_t (&a24)[L],
-                                            const F& f) {
-  uint32_t t1[L], t2[L], t3[L], t4[L], U[L], V[L], s[L], d[L];
-  f.add(t1, X0, Z0);
-  f.sub(t2, X0, Z0);
-  f.add(t3, X1, Z1);
-  f.sub(t4, X1, Z1);
-  f.mul(U, t2, t3);
-  f.mul(V, t1, t4);
-  f.sqr(s, t1);
-  f.sqr(d, t2);
-  f.mul(X0, s, d);
-  f.sub(t1, s, d);   // t
-  f.mul(t2, a24, t1); // a24 t
-  f.add(t2, d, t2);  // d + a24 t
-  f.mul(Z0, t1, t2);
-  f.add(t3, U, V);
-  f.sub(t4, U, V);
-  f.sqr(X1, t3);
-  f.sqr(t4, t4);
-  f.mul(Z1, x0, t4);
-}
-
-// The same step with a projective difference D = (Xd:Zd) (the paper-comparable prime-by-prime
-// schedule, reading G9b): X1' = Zd (U+V)^2, Z1' = Xd (U-V)^2 — 7M + 4S.
-template <int L, class F>
-__device__ __forceinline__ void ladder_step_d(uint32_t (&X0)[L], uint32_t (&Z0)[L], uint32_t (&X1)[L],
-                                              uint32_t (&Z1)[L], const uint32_t (&Xd)[L], const uint32_t (&Zd)[L],
-                                              const uint32_t (&a24)[L], const F& f) {
-  uint32_t t1[L], t2[L], t3[L], t4[L], U[L], V[L], s[L], d[L];
-  f.add(t1, X0, Z0);
-  f.sub(t2, X0, Z0);
-  f.add(t3, X1, Z1);
-  f.sub(t4, X1, Z1);
-  f.mul(U, t2, t3);
-  f.mul(V, t1, t4);
-  f.sqr(s, t1);
-  f.sqr(d, t2);
-  f.mul(X0, s, d);
-  f.sub(t1, s, d);
-  f.mul(t2, a24, t1);
-  f.add(t2, d, t2);
-  f.mul(Z0, t1, t2);
-  f.add(t3, U, V);
-  f.sub(t4, U, V);
-  f.sqr(t3, t3);
-  f.sqr(t4, t4);
-  f.mul(X1, Zd, t3);
-  f.mul(Z1, Xd, t4);
-}
-
-template <int L, class F>
-__device__ __forceinline__ void xdbl(uint32_t (&Xo)[L], uint32_t (&Zo)[L], const uint32_t (&X)[L], const uint32_t (&Z)[L],
-                                     const uint32_t (&a24)[L], const F& f) {
-  uint32_t t1[L], t2[L], sd[L], dd[L], tt[L];
-  f.add(t1, X, Z);
-  f.sub(t2, X, Z);
-  f.sqr(sd, t1);
-  f.sqr(dd, t2);
-  f.mul(Xo, sd, dd);
-  f.sub(tt, sd, dd);
-  f.mul(t1, a24, tt);
-  f.add(t1, dd, t1);
-  f.mul(Zo, tt, t1);
-}
-
-template <int L>
-__device__ __forceinline__ void cswap(uint32_t (&a)[L], uint32_t (&b)[L], bool c) {
-#pragma unroll
-  for (int k = 0; k < L; ++k) {
-    const uint32_t ta = c ? b[k] : a[k];
-    const uint32_t tb = c ? a[k] : b[k];
-    a[k] = ta;
-    b[k] = tb;
-  }
-}
-
-template <int L>
-__device__ __forceinline__ void store(uint32_t* dst, size_t i, const uint32_t (&v)[L]) {
-  if (!dst) return;
-  uint2* d2 = reinterpret_cast<uint2*>(dst + i * L);
-#pragma unroll
-  for (int k = 0; k < L / 2; ++k) d2[k] = make_uint2(v[2 * k], v[2 * k + 1]);
-}
-
-template <int L, int VAR, bool EAGER, bool PRIMES>
-__global__ void __launch_bounds__(kEcmTPB) ecm_stage1_kernel(const __grid_constant__ EcmParams p,
-                                                             const uint32_t* __restrict__ kwords, uint32_t k_bits,
-                                                             const uint64_t* __restrict__ sigmas, size_t count,
-                                                             uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status,
-                                                             uint32_t* xaff, uint32_t flags) {
-  const uint32_t(&N)[L] = cref<L>(p.N);
-  const uint32_t(&N2)[L] = cref<L>(p.N2);
-  const uint32_t(&R2)[L] = cref<L>(p.R2);
-  const uint32_t(&ONE)[L] = cref<L>(p.ONE);
-  const uint32_t(&NP)[L] = cref<L>(p.NP);
-  const uint32_t n0inv = p.n0inv;
-  const Field<L, VAR, EAGER> fld{N, EAGER ? N : N2, NP, n0inv};
-  const int lane = threadIdx.x & 31;
-  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = i < count;
-  const uint64_t sigma = live ? sigmas[i] : 6ull;
-
-  // ---------------- setup (Brent-Suyama) ----------------
-  uint32_t s[L], u[L], v[L], t[L], w[L], c[L];
-#pragma unroll
-  for (int k = 0; k < L; ++k) t[k] = 0;
-  t[0] = (uint32_t)sigma;
-  t[1] = (uint32_t)(sigma >> 32);
-  mont_mul<L>(s, t, R2, N, n0inv);                 // s = sigma R mod N (any sigma < 2^64)
-  // small Montgomery constants from ONE by lazy additions: 2, 4, 5, 3, 16
-  uint32_t two[L], four[L], five[L], three[L], sixteen[L];
-  add_lazy<L>(two, ONE, ONE, N2);
-  add_lazy<L>(four, two, two, N2);
-  add_lazy<L>(five, four, ONE, N2);
-  add_lazy<L>(three, two, ONE, N2);
-  add_lazy<L>(t, four, four, N2);
-  add_lazy<L>(sixteen, t, t, N2);
-  mont_mul<L>(t, s, s, N, n0inv);
-  sub_lazy<L>(u, t, five, N2);                     // u = s^2 - 5
-  add_lazy<L>(t, s, s, N2);
-  add_lazy<L>(v, t, t, N2);                        // v = 4 s
-  uint32_t u3[L], v3[L], D[L];
-  mont_mul<L>(t, u, u, N, n0inv);
-  mont_mul<L>(u3, t, u, N, n0inv);                 // u^3
-  mont_mul<L>(t, v, v, N, n0inv);
-  mont_mul<L>(v3, t, v, N, n0inv);                 // v^3
-  mont_mul<L>(t, sixteen, u3, N, n0inv);           // 16 u^3
-  mont_mul<L>(w, t, v3, N, n0inv);
-  mont_mul<L>(D, w, v, N, n0inv);                  // D = 16 u^3 v^4
-  // D out of Montgomery form, canonical, then invert
-  uint32_t Dn[L], gg[L], Di[L];
-#pragma unroll
-  for (int k = 0; k < L; ++k) c[k] = 0;
-  c[0] = 1;
-  mont_mul<L>(Dn, D, c, N, n0inv);
-  canonicalize<L>(Dn, Dn, N);
-  const bool ok = xgcd<L>(Dn, N, gg, Di);
-  uint8_t st;
-  uint32_t X0[L], Z0[L], X1[L], Z1[L], x0[L], a24[L];
-  if (ok) {
-    mont_mul<L>(w, Di, R2, N, n0inv);              // w = D^{-1} (Montgomery form)
-    // x0 = 16 u^3 * u^3 * v * w
-    mont_mul<L>(c, t, u3, N, n0inv);
-    mont_mul<L>(c, c, v, N, n0inv);
-    mont_mul<L>(x0, c, w, N, n0inv);
-    // a24 = (v-u)^3 (3u+v) v^3 w
-    sub_lazy<L>(t, v, u, N2);
-    mont_mul<L>(c, t, t, N, n0inv);
-    mont_mul<L>(c, c, t, N, n0inv);
-    mont_mul<L>(t, three, u, N, n0inv);
-    add_lazy<L>(t, t, v, N2);
-    mont_mul<L>(c, c, t, N, n0inv);
-    mont_mul<L>(c, c, v3, N, n0inv);
-    mont_mul<L>(a24, c, w, N, n0inv);
-    st = 0;
-  } else {
-    // gcd(D, N) == N (D == 0 mod N) -> 3; proper factor -> 4
-    st = equal(gg, N) ? 3 : 4;
-#pragma unroll
-    for (int k = 0; k < L; ++k) { x0[k] = 0; a24[k] = 0; }
-    copy(x0, ONE);  // keep the (discarded) ladder arithmetic well-defined
-  }
-
-  // ---------------- ladder over k (warp-uniform bits) ----------------
-  if (EAGER) {
-    canonicalize<L>(x0, x0, N);
-    canonicalize<L>(a24, a24, N);
-  }
-  copy(X0, x0);
-  copy(Z0, ONE);
-  if (!PRIMES) xdbl<L>(X1, Z1, X0, Z0, a24, fld);  // R1 = xDBL(P)
-  if (!PRIMES) {
-    bool swapped = false;
-    if (k_bits >= 2) {
-      int idx = (int)k_bits - 2;
-      int chunk = idx >> 10;  // 32 words = 1024 bits per warp-wide load
-      uint32_t kreg = kwords[(chunk << 5) + lane];
-      for (; idx >= 0; --idx) {
-        if ((idx >> 10) != chunk) {
-          chunk = idx >> 10;
-          kreg = kwords[(chunk << 5) + lane];
-        }
-        const uint32_t word = __shfl_sync(0xffffffffu, kreg, (idx >> 5) & 31);
-        const bool bit = (word >> (idx & 31)) & 1u;
-        // bit 1: (R0, R1) <- (xADD, xDBL(R1)); bit 0: (xDBL(R0), xADD).  Double the point in the
-        // (X0,Z0) slot: swap so that slot holds R_bit, swap back lazily on the next change.
-        cswap<L>(X0, X1, bit != swapped);
-        cswap<L>(Z0, Z1, bit != swapped);
-        swapped = bit;
-        ladder_step<L>(X0, Z0, X1, Z1, x0, a24, fld);
-      }
-    }
-    cswap<L>(X0, X1, swapped);
-    cswap<L>(Z0, Z1, swapped);
-  } else {
-    // prime-by-prime: kwords holds the list of primes p <= B1 (each repeated e_p times),
-    // k_bits its length; Q <- [p]Q by a ladder with difference Q for every entry.
-    uint32_t QX[L], QZ[L];
-    copy(QX, x0);
-    copy(QZ, ONE);
-    for (int c0 = 0; c0 < (int)k_bits; c0 += 32) {
-      const uint32_t preg = kwords[c0 + lane];
-      const int nt = ((int)k_bits - c0) < 32 ? ((int)k_bits - c0) : 32;
-      for (int t = 0; t < nt; ++t) {
-        const uint32_t pr = __shfl_sync(0xffffffffu, preg, t);
-        copy(X0, QX);
-        copy(Z0, QZ);
-        xdbl<L>(X1, Z1, QX, QZ, a24, fld);
-        bool swapped = false;
-        for (int i = 30 - __clz(pr); i >= 0; --i) {
-          const bool bit = (pr >> i) & 1u;
-          cswap<L>(X0, X1, bit != swapped);
-          cswap<L>(Z0, Z1, bit != swapped);
-          swapped = bit;
-          ladder_step_d<L>(X0, Z0, X1, Z1, QX, QZ, a24, fld);
-        }
-        cswap<L>(X0, X1, swapped);
-        cswap<L>(Z0, Z1, swapped);
-        copy(QX, X0);
-        copy(QZ, Z0);
-      }
-    }
-  }
-
-  // ---------------- tail: canonical X, Z; g = gcd(Z, N); affine x ----------------
-  if (!live) return;
-  uint32_t Xn[L], Zn[L], xa[L];
-#pragma unroll
-  for (int k = 0; k < L; ++k) { c[k] = 0; xa[k] = 0; }
-  c[0] = 1;
-  mont_mul<L>(Xn, X0, c, N, n0inv);
-  canonicalize<L>(Xn, Xn, N);
-  mont_mul<L>(Zn, Z0, c, N, n0inv);
-  canonicalize<L>(Zn, Zn, N);
-  if (st == 0) {
-    uint32_t Zi[L];
-    const bool inv = xgcd<L>(Zn, N, gg, Zi);
-    if (inv) {
-      st = 0;
-      if (xaff && !(flags & 0x20u)) {
-        mont_mul<L>(t, Xn, R2, N, n0inv);      // X R
-        mont_mul<L>(xa, t, Zi, N, n0inv);      // X Z^{-1}
-        canonicalize<L>(xa, xa, N);
-      }
-    } else {
-      st = equal(gg, N) ? 2 : 1;
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < L; ++k) { Xn[k] = 0; Zn[k] = 0; }
-  }
-  store<L>(X, i, Xn);
-  store<L>(Z, i, Zn);
-  store<L>(g, i, gg);
-  if (xaff && !(flags & 0x20u)) store<L>(xaff, i, xa);
-  status[i] = st;
-}
-
-template <int L, int VAR, bool EAGER, bool PRIMES = false>
-static cudaError_t launch_ecm_LV(const EcmParams& p, const uint32_t* kw, uint32_t k_bits, const uint64_t* sigmas,
-                                 size_t count, uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status, uint32_t* xaff,
-                                 uint32_t flags, cudaStream_t s) {
-  const size_t blocks = (count + kEcmTPB - 1) / kEcmTPB;
-  ecm_stage1_kernel<L, VAR, EAGER, PRIMES><<<(unsigned)blocks, kEcmTPB, 0, s>>>(p, kw, k_bits, sigmas, count, X, Z, g,
-                                                                        status, xaff, flags);
-  return cudaGetLastError();
-}
-
-// Ablation variants (REDC form x eager/lazy) are instantiated for L = 6 and 8 (192/256-bit,
-// the paper's 254-bit setting); every width gets the default lazy word-serial kernel.
-template <int L>
-static cudaError_t launch_ecm_L(const EcmParams& p, const uint32_t* kw, uint32_t k_bits, const uint64_t* sigmas,
-                                size_t count, uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status, uint32_t* xaff,
-                                uint32_t flags, cudaStream_t s) {
-  const uint32_t var = (flags >> 8) & 7u;
-  const bool eager = flags & 0x40u;
-  if (flags & 0x80u) {  // prime-by-prime schedule (paper-comparable)
-    if constexpr (L == 8) {
-#define ECM_PCASE(V, E) \
-      if (var == V && eager == E) return launch_ecm_LV<L, V, E, true>(p, kw, k_bits, sigmas, count, X, Z, g, status, xaff, flags, s);
-      ECM_PCASE(REDC_WORD, false)
-      ECM_PCASE(REDC_WORD, true)
-      ECM_PCASE(REDC_BLOCKTHM, false)
-      ECM_PCASE(REDC_BLOCKTHM, true)
-      ECM_PCASE(REDC_CLASSIC, false)
-      ECM_PCASE(REDC_CLASSIC, true)
-#undef ECM_PCASE
-    }
-    if constexpr (L == 6) {
-      if (var == REDC_WORD && !eager) return launch_ecm_LV<L, REDC_WORD, false, true>(p, kw, k_bits, sigmas, count, X, Z, g, status, xaff, flags, s);
-    }
-    return cudaErrorInvalidValue;
-  }
-  if (var == REDC_WORD && !eager) return launch_ecm_LV<L, REDC_WORD, false>(p, kw, k_bits, sigmas, count, X, Z, g, status, xaff, flags, s);
-  if constexpr (L == 6 || L == 8) {
-#define ECM_CASE(V, E) \
-    if (var == V && eager == E) return launch_ecm_LV<L, V, E>(p, kw, k_bits, sigmas, count, X, Z, g, status, xaff, flags, s);
-    ECM_CASE(REDC_WORD, true)
-    ECM_CASE(REDC_KNOWNLOW, false)
-    ECM_CASE(REDC_KNOWNLOW, true)
-    ECM_CASE(REDC_BLOCKTHM, false)
-    ECM_CASE(REDC_BLOCKTHM, true)
-    ECM_CASE(REDC_CLASSIC, false)
-    ECM_CASE(REDC_CLASSIC, true)
-#undef ECM_CASE
-  }
-  return cudaErrorInvalidValue;
-}
+cudaError_t launch_ecm_L(const EcmParams& p, const uint32_t* kw, uint32_t k_bits, const uint64_t* sigmas, size_t count,
+                         uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status, uint32_t* xaff, uint32_t flags,
+                         cudaStream_t s);
 
 cudaError_t launch_ecm(const EcmParams& p, const uint32_t* kw, uint32_t k_bits, const uint64_t* sigmas, size_t count,
                        uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status, uint32_t* xaff, uint32_t flags,

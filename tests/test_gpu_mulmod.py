@@ -65,6 +65,24 @@ def lt_2n(x, n):
 @pytest.mark.parametrize("L", (4, 6, 8, 12, 16))
 @pytest.mark.parametrize("square", (False, True))
 @pytest.mark.parametrize("layout", ("aos", "sliced"))
+@pytest.mark.parametrize("kernel", ("stream", "warp"))
+def test_parity_both_kernels(orc, torch, L, square, layout, kernel):
+    # the CTA-tile streaming kernel (bulk-copy ring of 256-element tiles, ragged tail by direct
+    # loads) and the warp-tile kernel, each forced at short and long chains; counts: several
+    # full CTA tiles + a ragged tail (count % 4 == 0 keeps sliced rows on the bulk path), an
+    # exact multiple of the tile, and a count below one tile (tail only)
+    flags = ((eg.ECM_SQUARE if square else 0) | (eg.ECM_LAYOUT_SLICED if layout == "sliced" else 0) |
+             (eg.ECM_KERNEL_STREAM if kernel == "stream" else eg.ECM_KERNEL_WARP))
+    for count, iters in ((256 * 9 + 100, 1), (256 * 4, 3), (60, 2), (256 * 3 + 4, 16)):
+        a, b, n = mulmod_inputs(count, L, seed=300 + L + count, lazy=True)
+        got = run_gpu(torch, a, b, n, L, iters, flags)
+        want = orc.mulmod_chain_mt(a, b, n, L, iters, square=square)
+        assert np.array_equal(got, want), (L, square, layout, kernel, count, iters)
+
+
+@pytest.mark.parametrize("L", (4, 6, 8, 12, 16))
+@pytest.mark.parametrize("square", (False, True))
+@pytest.mark.parametrize("layout", ("aos", "sliced"))
 def test_parity_small_all_widths(orc, torch, L, square, layout):
     # several tiles and a ragged tail; 32*37+4 keeps sliced rows 16-byte aligned (vector path),
     # 32*37+5 does not (scalar path)
@@ -155,8 +173,10 @@ def test_c2_full_size(orc, torch):
     idx = np.arange(0, count, count // (1 << 14)) + 13
     want = orc.mulmod_chain_mt(a[idx], b[idx], n[idx], L, 256)
     assert np.array_equal(got[idx], want)
-    # the same triples in the limb-sliced layout give the same outputs
+    # the same triples in the limb-sliced layout give the same outputs (K = 1: streaming kernel)
     S = [dev(torch, x.T.copy()) for x in (a, b, n)]
+    g1 = eg.ecm_mulmod_batch(*S, L=L, iters=1, flags=eg.ECM_LAYOUT_SLICED).cpu().numpy().T
+    assert np.array_equal(g1, orc.mulmod_chain_mt(a, b, n, L, 1))
     gs = eg.ecm_mulmod_batch(*S, L=L, iters=256, flags=eg.ECM_LAYOUT_SLICED).cpu().numpy().T
     assert np.array_equal(gs, got)
 
@@ -173,3 +193,31 @@ def test_host_buffers_pipelined_multichunk(orc, torch):
     assert np.array_equal(out.numpy(), want)
     sq = eg.ecm_mulmod_batch(a, b, n, L=L, iters=2, flags=eg.ECM_HOST_BUFFERS | eg.ECM_SQUARE)
     assert np.array_equal(sq, orc.mulmod_chain_mt(a, b, n, L, 2, square=True))
+
+
+def test_host_buffers_pipelined_sliced(orc, torch):
+    """ECM_HOST_BUFFERS | ECM_LAYOUT_SLICED: chunks move as 2-D copies of L rows; the ragged last
+    chunk (count % 4 != 0) takes the warp-tile kernel."""
+    L = 6
+    count = (1 << 19) + 77
+    a, b, n = mulmod_inputs(count, L, seed=11, lazy=True)
+    sa, sb, sn = (torch.from_numpy(x.T.copy()).pin_memory() for x in (a, b, n))
+    out = torch.empty_like(sa).pin_memory()
+    for iters in (1, 5):
+        eg.ecm_mulmod_batch(sa, sb, sn, out, L=L, iters=iters, flags=eg.ECM_HOST_BUFFERS | eg.ECM_LAYOUT_SLICED)
+        want = orc.mulmod_chain_mt(a, b, n, L, iters)
+        assert np.array_equal(out.numpy().T, want), iters
+
+
+def test_stream_kernel_in_place(orc, torch):
+    """out may alias a (include/ecmgpu.h): the streaming kernel's prefetch never reads a tile
+    after its output was stored."""
+    L = 8
+    count = 256 * 40 + 36
+    a, b, n = mulmod_inputs(count, L, seed=12, lazy=True)
+    want = orc.mulmod_chain_mt(a, b, n, L, 2)
+    for fl, tr in ((0, False), (eg.ECM_LAYOUT_SLICED, True)):
+        A, B, Nn = (dev(torch, x.T.copy() if tr else x) for x in (a, b, n))
+        eg.ecm_mulmod_batch(A, B, Nn, A, L=L, iters=2, flags=fl | eg.ECM_KERNEL_STREAM)
+        got = A.cpu().numpy()
+        assert np.array_equal(got.T if tr else got, want), fl
