@@ -152,27 +152,42 @@ def ncu_traffic(name):
 
 
 # ---------------------------------------------------------------------------------------
-def cpu_baseline_mulmod(sample_elems: int, iters: int):
+CPU_TARGET_S = 10.0  # bounded oracle sample: about 10 s of host work per baseline
+
+
+def cpu_baseline_mulmod(sample_elems: int, iters: int, target_s: float = CPU_TARGET_S):
+    """The oracle as it stands on all host cores, over consecutive C2 triples: at least
+    `sample_elems`, then further chunks until about `target_s` seconds have elapsed."""
     import oracle
     from workload import mulmod_inputs
-    a, b, n = mulmod_inputs(sample_elems, L, seed=2)
     threads = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    oracle.mulmod_chain_mt(a, b, n, L, iters, threads=threads)
-    dt = time.perf_counter() - t0
-    return {"value": sample_elems * iters / dt, "unit": "modmul/s", "cores": threads, "kind": "oracle",
-            "sample": f"first {sample_elems} of C2's 2^24 triples x K={iters} (oracle C, {threads} host threads)",
+    done, dt = 0, 0.0
+    while done < C2_COUNT and (done < sample_elems or dt < target_s):
+        chunk = sample_elems if done == 0 else min(max(threads * 2048, sample_elems), C2_COUNT - done)
+        a, b, n = mulmod_inputs(chunk, L, seed=2, start=done)
+        t0 = time.perf_counter()
+        oracle.mulmod_chain_mt(a, b, n, L, iters, threads=threads)
+        dt += time.perf_counter() - t0
+        done += chunk
+    return {"value": done * iters / dt, "unit": "modmul/s", "cores": threads, "kind": "oracle",
+            "sample": f"first {done} of C2's 2^24 triples x K={iters} (oracle C, {threads} host threads)",
             "seconds": dt}
 
 
-def cpu_baseline_ecm(N, k, sigmas, B1):
+def cpu_baseline_ecm(N, k, sigmas, B1, target_s: float = CPU_TARGET_S):
+    """The oracle on all host cores over a strided sample of C3's curves, in chunks of one
+    curve per thread until about `target_s` seconds have elapsed (or the sample is used up)."""
     import oracle
     threads = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    oracle.ecm_stage1_mt(N, L, k, sigmas, threads=threads)
-    dt = time.perf_counter() - t0
-    return {"value": len(sigmas) / dt, "unit": "curves/s", "cores": threads, "kind": "oracle",
-            "sample": f"{len(sigmas)} of C3's curves at B1={B1}", "seconds": dt}
+    done, dt = 0, 0.0
+    while done < len(sigmas) and dt < target_s:
+        part = sigmas[done:done + threads]
+        t0 = time.perf_counter()
+        oracle.ecm_stage1_mt(N, L, k, part, threads=threads)
+        dt += time.perf_counter() - t0
+        done += len(part)
+    return {"value": done / dt, "unit": "curves/s", "cores": threads, "kind": "oracle",
+            "sample": f"{done} strided curves of C3 at B1={B1}", "seconds": dt}
 
 
 # ---------------------------------------------------------------------------------------
@@ -396,13 +411,13 @@ def run_ours(args):
             par["ecm_checked"] = int(len(ci))
             par["ecm_mismatches"] = int(((g3 != w3["g"]).any(axis=1) | (s3 != w3["status"])).sum())
         line["parity"] = par
-        line["cpu_baseline"] = cpu_baseline_mulmod(args.cpu_elems, args.iters)
+        line["cpu_baseline"] = cpu_baseline_mulmod(args.cpu_elems, args.iters, target_s=args.cpu_seconds)
         if ecm:
             cfg = ecm_config("C3")
             import oracle
             k, _ = oracle.stage1_k(cfg["B1"])
             idx = np.arange(0, cfg["curves"], cfg["curves"] // args.cpu_curves)[: args.cpu_curves]
-            ecm["cpu_baseline"] = cpu_baseline_ecm(cfg["N"], k, cfg["sigmas"][idx], cfg["B1"])
+            ecm["cpu_baseline"] = cpu_baseline_ecm(cfg["N"], k, cfg["sigmas"][idx], cfg["B1"], target_s=args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -417,11 +432,11 @@ def run_reference(args):
         return
     sample = args.cpu_elems
     for _ in range(args.warmup):
-        cpu_baseline_mulmod(max(1024, sample // 16), args.iters)
+        cpu_baseline_mulmod(max(1024, sample // 16), args.iters, target_s=0.0)
     vals = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(cpu_baseline_mulmod(sample, args.iters))
+        vals.append(cpu_baseline_mulmod(sample, args.iters, target_s=0.0))
     dt = time.perf_counter() - t0
     value = sample * args.iters * args.steps / dt
     cb = dict(vals[-1])
@@ -451,7 +466,8 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--c5", action="store_true", help="also time one rank's 1/8 shard of C5 (~40 s)")
     ap.add_argument("--cpu-elems", type=int, default=1 << 17)
-    ap.add_argument("--cpu-curves", type=int, default=64)
+    ap.add_argument("--cpu-curves", type=int, default=4096, help="strided C3 curves available to the oracle")
+    ap.add_argument("--cpu-seconds", type=float, default=CPU_TARGET_S, help="host seconds per oracle baseline")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -21,7 +21,7 @@ def _one_line(out):
 
 def test_bench_single_rank_small():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *SMALL, "--cpu-elems", "2048",
-                        "--cpu-curves", "8"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+                        "--cpu-curves", "8", "--cpu-seconds", "0.5"], capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     d = _one_line(r.stdout)
     assert d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] == 2

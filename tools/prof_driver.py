@@ -20,12 +20,14 @@ ap.add_argument("--flags", type=int, default=0)
 ap.add_argument("--curves", type=int, default=1 << 16)
 ap.add_argument("--B1", type=int, default=50000)
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--sliced", action="store_true", help="limb-sliced layout (the bench headline)")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 if a.what == "mulmod":
-    x, y, n = (torch.from_numpy(v).cuda() for v in mulmod_inputs(a.count, a.L, seed=2))
+    x, y, n = (torch.from_numpy(v.T.copy() if a.sliced else v).cuda() for v in mulmod_inputs(a.count, a.L, seed=2))
+    fl = a.flags | (eg.ECM_LAYOUT_SLICED if a.sliced else 0)
     for _ in range(a.reps):
-        eg.ecm_mulmod_batch(x, y, n, L=a.L, iters=a.iters, flags=a.flags)
+        eg.ecm_mulmod_batch(x, y, n, L=a.L, iters=a.iters, flags=fl)
 else:
     cfg = ecm_config("C3")
     s = torch.from_numpy(cfg["sigmas"][: a.curves].copy()).cuda()

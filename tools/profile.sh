@@ -19,9 +19,11 @@ cap() {  # name kernel-regex driver-args...
   ncu -i /tmp/${TAG}_$name.ncu-rep --page source --csv > $OUT/${TAG}_ncu_${name}_source.csv 2>/dev/null
   rm -f /tmp/${TAG}_$name.ncu-rep
 }
-cap mulmod mulmod_batch_kernel mulmod --reps 1
-cap sqr mulmod_batch_kernel mulmod --flags 2 --reps 1
-cap k1 mulmod_batch_kernel mulmod --iters 1 --reps 1
+cap mulmod mulmod_batch_kernel mulmod --sliced --reps 1
+cap mulmod_aos mulmod_batch_kernel mulmod --reps 1
+cap sqr mulmod_batch_kernel mulmod --sliced --flags 2 --reps 1
+cap k1 mulmod_ mulmod --iters 1 --reps 1
+cap k1_sliced mulmod_ mulmod --sliced --iters 1 --reps 1
 cap ecm ecm_stage1_kernel ecm --curves 1048576 --B1 2000 --reps 1
 fi
 ls -la $OUT
