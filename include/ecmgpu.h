@@ -81,6 +81,13 @@ typedef enum {
    back to the warp-tile kernel unless count % 4 == 0 and every array is 16-byte aligned. */
 #define ECM_KERNEL_STREAM 0x800u
 #define ECM_KERNEL_WARP 0x1000u
+/* stage 1 kernel choice (diagnostic; the default picks by batch size): one curve
+   per thread (throughput kernel) or four lanes per curve (latency kernel: the ladder step's 10
+   products as three rounds of independent products spread over the lanes of a 4-lane group,
+   default for count <= 64 x SMs).  Outputs are identical.  LANES4 needs the default REDC_WORD
+   lazy full-k ladder (ECM_E_ARG with ECM_EAGER, ECM_PRIME_LADDERS or another REDC variant). */
+#define ECM_KERNEL_LANES4 0x2000u
+#define ECM_KERNEL_LANES1 0x4000u
 
 /* Status values written per curve by ecm_stage1_batch / ecm_ladder_batch. */
 #define ECM_CURVE_NO_FACTOR 0    /* g == 1 */

@@ -25,6 +25,20 @@
 namespace ecm {
 
 constexpr int kEcmTPB = 128;
+// Build-time experiment knobs (tools/ecm_ab.py builds variant libraries; defaults = the product):
+//   ECM_MIN_BLOCKS  : __launch_bounds__ min CTAs/SM for the ladder kernel (0 = unconstrained)
+//   ECM_SWAP_BRANCH : 1 = no conditional swap; a warp-uniform branch picks which slot is doubled
+#ifndef ECM_MIN_BLOCKS
+#define ECM_MIN_BLOCKS -1  // -1: ecm_min_blocks' per-instantiation default
+#endif
+#ifndef ECM_SWAP_BRANCH
+#define ECM_SWAP_BRANCH 0
+#endif
+// The default L <= 6 ladder is held to 80 registers = 6 CTAs x 4 warps per SM (at 81..88 the
+// 256-register warp allocation granule leaves 5); the cap costs one spill load per step.
+__host__ __device__ constexpr int ecm_min_blocks(int L, int V, bool eager, bool primes) {
+  return ECM_MIN_BLOCKS >= 0 ? ECM_MIN_BLOCKS : (L <= 6 && V == 0 && !eager && !primes) ? 6 : 0;
+}
 
 template <int L>
 __device__ __forceinline__ const uint32_t (&cref(const uint32_t* p))[L] {
@@ -273,25 +287,18 @@ __device__ __forceinline__ void store(uint32_t* dst, size_t i, const uint32_t (&
   for (int k = 0; k < L / 2; ++k) d2[k] = make_uint2(v[2 * k], v[2 * k + 1]);
 }
 
-template <int L, int VAR, bool EAGER, bool PRIMES>
-__global__ void __launch_bounds__(kEcmTPB) ecm_stage1_kernel(const __grid_constant__ EcmParams p,
-                                                             const uint32_t* __restrict__ kwords, uint32_t k_bits,
-                                                             const uint64_t* __restrict__ sigmas, size_t count,
-                                                             uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status,
-                                                             uint32_t* xaff, uint32_t flags) {
+// ---------------------------------------------------------------------------------------
+// Setup (Brent-Suyama, reading G10): sigma -> (x0, a24) in Montgomery form; gg = gcd(D, N) when
+// the setup denominator D = 16 u^3 v^4 is not invertible (status 3 / 4).
+// ---------------------------------------------------------------------------------------
+template <int L>
+__device__ __forceinline__ uint8_t ecm_setup(const EcmParams& p, uint64_t sigma, uint32_t (&x0)[L], uint32_t (&a24)[L],
+                                             uint32_t (&gg)[L]) {
   const uint32_t(&N)[L] = cref<L>(p.N);
   const uint32_t(&N2)[L] = cref<L>(p.N2);
   const uint32_t(&R2)[L] = cref<L>(p.R2);
   const uint32_t(&ONE)[L] = cref<L>(p.ONE);
-  const uint32_t(&NP)[L] = cref<L>(p.NP);
   const uint32_t n0inv = p.n0inv;
-  const Field<L, VAR, EAGER> fld{N, EAGER ? N : N2, NP, n0inv};
-  const int lane = threadIdx.x & 31;
-  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = i < count;
-  const uint64_t sigma = live ? sigmas[i] : 6ull;
-
-  // ---------------- setup (Brent-Suyama) ----------------
   uint32_t s[L], u[L], v[L], t[L], w[L], c[L];
 #pragma unroll
   for (int k = 0; k < L; ++k) t[k] = 0;
@@ -319,7 +326,7 @@ __global__ void __launch_bounds__(kEcmTPB) ecm_stage1_kernel(const __grid_consta
   mont_mul<L>(w, t, v3, N, n0inv);
   mont_mul<L>(D, w, v, N, n0inv);                  // D = 16 u^3 v^4
   // D out of Montgomery form, canonical, then invert
-  uint32_t Dn[L], gg[L], Di[L];
+  uint32_t Dn[L], Di[L];
 #pragma unroll
   for (int k = 0; k < L; ++k) c[k] = 0;
   c[0] = 1;
@@ -327,7 +334,6 @@ __global__ void __launch_bounds__(kEcmTPB) ecm_stage1_kernel(const __grid_consta
   canonicalize<L>(Dn, Dn, N);
   const bool ok = xgcd<L>(Dn, N, gg, Di);
   uint8_t st;
-  uint32_t X0[L], Z0[L], X1[L], Z1[L], x0[L], a24[L];
   if (ok) {
     mont_mul<L>(w, Di, R2, N, n0inv);              // w = D^{-1} (Montgomery form)
     // x0 = 16 u^3 * u^3 * v * w
@@ -352,6 +358,86 @@ __global__ void __launch_bounds__(kEcmTPB) ecm_stage1_kernel(const __grid_consta
     copy(x0, ONE);  // keep the (discarded) ladder arithmetic well-defined
   }
 
+  return st;
+}
+
+// setup, and g = gcd(D, N) of a curve whose setup failed written at once (ecm_tail skips it)
+template <int L>
+__device__ __forceinline__ uint8_t ecm_setup_store(const EcmParams& p, uint64_t sigma, uint32_t (&x0)[L],
+                                                   uint32_t (&a24)[L], bool live, size_t i, uint32_t* g) {
+  uint32_t gg[L];
+  const uint8_t st = ecm_setup<L>(p, sigma, x0, a24, gg);
+  if (live && st != 0) store<L>(g, i, gg);
+  return st;
+}
+
+// ---------------------------------------------------------------------------------------
+// Tail: X, Z out of Montgomery form and canonical; g = gcd(Z, N) and Z^{-1} by one binary xgcd;
+// status; affine x = X Z^{-1}.  Writes curve i's outputs.
+// ---------------------------------------------------------------------------------------
+// A curve whose setup failed (st = 3 / 4) had its g written by ecm_setup_store already, so the
+// setup gcd is not live across the ladder.
+template <int L>
+__device__ __forceinline__ void ecm_tail(const EcmParams& p, const uint32_t (&X0)[L], const uint32_t (&Z0)[L], uint8_t st,
+                                         size_t i, uint32_t* X, uint32_t* Z, uint32_t* g,
+                                         uint8_t* status, uint32_t* xaff, uint32_t flags) {
+  uint32_t gg[L];
+  const uint32_t(&N)[L] = cref<L>(p.N);
+  const uint32_t(&R2)[L] = cref<L>(p.R2);
+  const uint32_t n0inv = p.n0inv;
+  uint32_t c[L], t[L];
+  uint32_t Xn[L], Zn[L], xa[L];
+#pragma unroll
+  for (int k = 0; k < L; ++k) { c[k] = 0; xa[k] = 0; }
+  c[0] = 1;
+  mont_mul<L>(Xn, X0, c, N, n0inv);
+  canonicalize<L>(Xn, Xn, N);
+  mont_mul<L>(Zn, Z0, c, N, n0inv);
+  canonicalize<L>(Zn, Zn, N);
+  if (st == 0) {
+    uint32_t Zi[L];
+    const bool inv = xgcd<L>(Zn, N, gg, Zi);
+    if (inv) {
+      st = 0;
+      if (xaff && !(flags & 0x20u)) {
+        mont_mul<L>(t, Xn, R2, N, n0inv);      // X R
+        mont_mul<L>(xa, t, Zi, N, n0inv);      // X Z^{-1}
+        canonicalize<L>(xa, xa, N);
+      }
+    } else {
+      st = equal(gg, N) ? 2 : 1;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < L; ++k) { Xn[k] = 0; Zn[k] = 0; }
+  }
+  store<L>(X, i, Xn);
+  store<L>(Z, i, Zn);
+  if (st <= 2) store<L>(g, i, gg);
+  if (xaff && !(flags & 0x20u)) store<L>(xaff, i, xa);
+  status[i] = st;
+}
+
+template <int L, int VAR, bool EAGER, bool PRIMES>
+__global__ void __launch_bounds__(kEcmTPB, ecm_min_blocks(L, VAR, EAGER, PRIMES)) ecm_stage1_kernel(const __grid_constant__ EcmParams p,
+                                                             const uint32_t* __restrict__ kwords, uint32_t k_bits,
+                                                             const uint64_t* __restrict__ sigmas, size_t count,
+                                                             uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status,
+                                                             uint32_t* xaff, uint32_t flags) {
+  const uint32_t(&N)[L] = cref<L>(p.N);
+  const uint32_t(&N2)[L] = cref<L>(p.N2);
+  const uint32_t(&ONE)[L] = cref<L>(p.ONE);
+  const uint32_t(&NP)[L] = cref<L>(p.NP);
+  const uint32_t n0inv = p.n0inv;
+  const Field<L, VAR, EAGER> fld{N, EAGER ? N : N2, NP, n0inv};
+  const int lane = threadIdx.x & 31;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = i < count;
+  const uint64_t sigma = live ? sigmas[i] : 6ull;
+
+  uint32_t X0[L], Z0[L], X1[L], Z1[L], x0[L], a24[L];
+  const uint8_t st = ecm_setup_store<L>(p, sigma, x0, a24, live, i, g);
+
   // ---------------- ladder over k (warp-uniform bits) ----------------
   if (EAGER) {
     canonicalize<L>(x0, x0, N);
@@ -373,12 +459,19 @@ __global__ void __launch_bounds__(kEcmTPB) ecm_stage1_kernel(const __grid_consta
         }
         const uint32_t word = __shfl_sync(0xffffffffu, kreg, (idx >> 5) & 31);
         const bool bit = (word >> (idx & 31)) & 1u;
+#if ECM_SWAP_BRANCH
+        // bit 1: R1 <- xDBL(R1), R0 <- xADD(R0, R1); bit 0: R0 <- xDBL(R0), R1 <- xADD.  The
+        // bit is warp-uniform, so this is a uniform branch between two copies of the step.
+        if (bit) ladder_step<L>(X1, Z1, X0, Z0, x0, a24, fld);
+        else ladder_step<L>(X0, Z0, X1, Z1, x0, a24, fld);
+#else
         // bit 1: (R0, R1) <- (xADD, xDBL(R1)); bit 0: (xDBL(R0), xADD).  Double the point in the
         // (X0,Z0) slot: swap so that slot holds R_bit, swap back lazily on the next change.
         cswap<L>(X0, X1, bit != swapped);
         cswap<L>(Z0, Z1, bit != swapped);
         swapped = bit;
         ladder_step<L>(X0, Z0, X1, Z1, x0, a24, fld);
+#endif
       }
     }
     cswap<L>(X0, X1, swapped);
@@ -413,44 +506,156 @@ __global__ void __launch_bounds__(kEcmTPB) ecm_stage1_kernel(const __grid_consta
     }
   }
 
-  // ---------------- tail: canonical X, Z; g = gcd(Z, N); affine x ----------------
   if (!live) return;
-  uint32_t Xn[L], Zn[L], xa[L];
-#pragma unroll
-  for (int k = 0; k < L; ++k) { c[k] = 0; xa[k] = 0; }
-  c[0] = 1;
-  mont_mul<L>(Xn, X0, c, N, n0inv);
-  canonicalize<L>(Xn, Xn, N);
-  mont_mul<L>(Zn, Z0, c, N, n0inv);
-  canonicalize<L>(Zn, Zn, N);
-  if (st == 0) {
-    uint32_t Zi[L];
-    const bool inv = xgcd<L>(Zn, N, gg, Zi);
-    if (inv) {
-      st = 0;
-      if (xaff && !(flags & 0x20u)) {
-        mont_mul<L>(t, Xn, R2, N, n0inv);      // X R
-        mont_mul<L>(xa, t, Zi, N, n0inv);      // X Z^{-1}
-        canonicalize<L>(xa, xa, N);
-      }
-    } else {
-      st = equal(gg, N) ? 2 : 1;
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < L; ++k) { Xn[k] = 0; Zn[k] = 0; }
-  }
-  store<L>(X, i, Xn);
-  store<L>(Z, i, Zn);
-  store<L>(g, i, gg);
-  if (xaff && !(flags & 0x20u)) store<L>(xaff, i, xa);
-  status[i] = st;
+  ecm_tail<L>(p, X0, Z0, st, i, X, Z, g, status, xaff, flags);
 }
+
+// ---------------------------------------------------------------------------------------
+// Latency kernel: four lanes per curve (small batches, e.g. C1's 256 curves, where one warp per
+// SM sub-partition leaves the one-curve-per-thread ladder bound by dependency latency).  The 10
+// products of a ladder step form three rounds of independent products (4, 4, 2); lane q of the
+// curve's 4-lane group computes product q of each round and the group exchanges the results
+// with __shfl_sync (width 4).  The additions, the swap and the scalar bits are replicated in all
+// four lanes, so every lane holds the whole state and every instruction stays warp-uniform.
+// Squares go through the multiply (mont_mul(x, x) == mont_sqr(x), the unique raw REDC value), so
+// the outputs are bit-identical to ecm_stage1_kernel's.
+// ---------------------------------------------------------------------------------------
+constexpr int kCoopLanes = 4;
+constexpr int kCoopTPB = 128;
+
+// d = a_q, branch-free (lanes of a warp hold different q): bit masks of q, 3 LOP3 per word
+template <int L>
+__device__ __forceinline__ void pick4(uint32_t (&d)[L], int q, const uint32_t (&a0)[L], const uint32_t (&a1)[L],
+                                      const uint32_t (&a2)[L], const uint32_t (&a3)[L]) {
+  const uint32_t m1 = 0u - (uint32_t)(q & 1), m2 = 0u - (uint32_t)((q >> 1) & 1);
+#pragma unroll
+  for (int k = 0; k < L; ++k) {
+    const uint32_t lo = (a0[k] & ~m1) | (a1[k] & m1);
+    const uint32_t hi = (a2[k] & ~m1) | (a3[k] & m1);
+    d[k] = (lo & ~m2) | (hi & m2);
+  }
+}
+
+template <int L>
+__device__ __forceinline__ void from_lane(uint32_t (&d)[L], const uint32_t (&r)[L], int q) {
+#pragma unroll
+  for (int k = 0; k < L; ++k) d[k] = __shfl_sync(0xffffffffu, r[k], q, kCoopLanes);
+}
+
+template <int L>
+__device__ __forceinline__ void ladder_step_coop(uint32_t (&X0)[L], uint32_t (&Z0)[L], uint32_t (&X1)[L],
+                                                 uint32_t (&Z1)[L], const uint32_t (&x0)[L], const uint32_t (&a24)[L],
+                                                 const uint32_t (&N)[L], const uint32_t (&N2)[L], uint32_t n0inv,
+                                                 int q) {
+  uint32_t t1[L], t2[L], t3[L], t4[L], a[L], b[L], r[L];
+  add_lazy<L>(t1, X0, Z0, N2);
+  sub_lazy<L>(t2, X0, Z0, N2);
+  add_lazy<L>(t3, X1, Z1, N2);
+  sub_lazy<L>(t4, X1, Z1, N2);
+  // round A: U = t2 t3, V = t1 t4, s = t1^2, d = t2^2
+  pick4<L>(a, q, t2, t1, t1, t2);
+  pick4<L>(b, q, t3, t4, t1, t2);
+  mont_mul<L>(r, a, b, N, n0inv);
+  uint32_t U[L], V[L], sd[L], dd[L];
+  from_lane<L>(U, r, 0);
+  from_lane<L>(V, r, 1);
+  from_lane<L>(sd, r, 2);
+  from_lane<L>(dd, r, 3);
+  uint32_t tt[L], w1[L], w2[L];
+  sub_lazy<L>(tt, sd, dd, N2);  // t = s - d
+  add_lazy<L>(w1, U, V, N2);
+  sub_lazy<L>(w2, U, V, N2);
+  // round B: X0' = s d, a24 t, X1' = (U+V)^2, (U-V)^2
+  pick4<L>(a, q, sd, a24, w1, w2);
+  pick4<L>(b, q, dd, tt, w1, w2);
+  mont_mul<L>(r, a, b, N, n0inv);
+  uint32_t at[L], sq[L];
+  from_lane<L>(X0, r, 0);
+  from_lane<L>(at, r, 1);
+  from_lane<L>(X1, r, 2);
+  from_lane<L>(sq, r, 3);
+  add_lazy<L>(w1, dd, at, N2);  // d + a24 t
+  // round C: Z0' = t (d + a24 t), Z1' = x0 (U-V)^2 (lanes 2, 3 repeat lanes 0, 1)
+  pick4<L>(a, q, tt, x0, tt, x0);
+  pick4<L>(b, q, w1, sq, w1, sq);
+  mont_mul<L>(r, a, b, N, n0inv);
+  from_lane<L>(Z0, r, 0);
+  from_lane<L>(Z1, r, 1);
+}
+
+template <int L>
+__global__ void __launch_bounds__(kCoopTPB) ecm_stage1_coop_kernel(const __grid_constant__ EcmParams p,
+                                                                   const uint32_t* __restrict__ kwords, uint32_t k_bits,
+                                                                   const uint64_t* __restrict__ sigmas, size_t count,
+                                                                   uint32_t* X, uint32_t* Z, uint32_t* g,
+                                                                   uint8_t* status, uint32_t* xaff, uint32_t flags) {
+  const uint32_t(&N)[L] = cref<L>(p.N);
+  const uint32_t(&N2)[L] = cref<L>(p.N2);
+  const uint32_t(&ONE)[L] = cref<L>(p.ONE);
+  const uint32_t(&NP)[L] = cref<L>(p.NP);
+  const uint32_t n0inv = p.n0inv;
+  const Field<L, REDC_WORD, false> fld{N, N2, NP, n0inv};
+  const int lane = threadIdx.x & 31;
+  const int q = lane & (kCoopLanes - 1);
+  const size_t i = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) / kCoopLanes;
+  const bool live = i < count;
+  const uint64_t sigma = live ? sigmas[i] : 6ull;
+
+  uint32_t X0[L], Z0[L], X1[L], Z1[L], x0[L], a24[L];
+  const uint8_t st = ecm_setup_store<L>(p, sigma, x0, a24, live, i, g);
+  copy(X0, x0);
+  copy(Z0, ONE);
+  xdbl<L>(X1, Z1, X0, Z0, a24, fld);  // R1 = xDBL(P), replicated
+  bool swapped = false;
+  if (k_bits >= 2) {
+    int idx = (int)k_bits - 2;
+    int chunk = idx >> 10;
+    uint32_t kreg = kwords[(chunk << 5) + lane];
+    for (; idx >= 0; --idx) {
+      if ((idx >> 10) != chunk) {
+        chunk = idx >> 10;
+        kreg = kwords[(chunk << 5) + lane];
+      }
+      const uint32_t word = __shfl_sync(0xffffffffu, kreg, (idx >> 5) & 31);
+      const bool bit = (word >> (idx & 31)) & 1u;
+      cswap<L>(X0, X1, bit != swapped);
+      cswap<L>(Z0, Z1, bit != swapped);
+      swapped = bit;
+      ladder_step_coop<L>(X0, Z0, X1, Z1, x0, a24, N, N2, n0inv, q);
+    }
+  }
+  cswap<L>(X0, X1, swapped);
+  cswap<L>(Z0, Z1, swapped);
+  if (!live || q != 0) return;
+  ecm_tail<L>(p, X0, Z0, st, i, X, Z, g, status, xaff, flags);
+}
+
+// Batches up to this many curves per SM take the 4-lane kernel by default: below ~80 curves/SM
+// (≈2.6 four-lane warps per SM sub-partition) it beats the one-lane kernel, which stays
+// latency-bound up to one warp per sub-partition (profiles/r01_ecm_lat.jsonl).
+constexpr size_t kCoopMaxCurvesPerSM = 64;
 
 template <int L, int VAR, bool EAGER, bool PRIMES = false>
 static cudaError_t launch_ecm_LV(const EcmParams& p, const uint32_t* kw, uint32_t k_bits, const uint64_t* sigmas,
                                  size_t count, uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status, uint32_t* xaff,
                                  uint32_t flags, cudaStream_t s) {
+  if (VAR == REDC_WORD && !EAGER && !PRIMES && !(flags & 0x4000u)) {
+    bool coop = (flags & 0x2000u) != 0;  // ECM_KERNEL_LANES4 forces it, ECM_KERNEL_LANES1 forbids it
+    if (!coop) {
+      int dev = 0, sms = 0;
+      cudaError_t e = cudaGetDevice(&dev);
+      if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (e != cudaSuccess) return e;
+      coop = count <= (size_t)sms * kCoopMaxCurvesPerSM;
+    }
+    if (coop) {
+      const size_t threads = count * kCoopLanes;
+      const size_t blocks = (threads + kCoopTPB - 1) / kCoopTPB;
+      ecm_stage1_coop_kernel<L><<<(unsigned)blocks, kCoopTPB, 0, s>>>(p, kw, k_bits, sigmas, count, X, Z, g, status,
+                                                                      xaff, flags);
+      return cudaGetLastError();
+    }
+  }
   const size_t blocks = (count + kEcmTPB - 1) / kEcmTPB;
   ecm_stage1_kernel<L, VAR, EAGER, PRIMES><<<(unsigned)blocks, kEcmTPB, 0, s>>>(p, kw, k_bits, sigmas, count, X, Z, g,
                                                                         status, xaff, flags);

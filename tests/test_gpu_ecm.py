@@ -35,10 +35,16 @@ def assert_same(got, want, keys=("X", "Z", "g", "status", "xaff")):
         assert np.array_equal(got[k], want[k]), k
 
 
-def test_c1_all_curves_bit_exact(orc, torch):
+KERNELS = {"default": 0, "lanes1": eg.ECM_KERNEL_LANES1, "lanes4": eg.ECM_KERNEL_LANES4}
+
+
+@pytest.mark.parametrize("kernel", list(KERNELS))
+def test_c1_all_curves_bit_exact(orc, torch, kernel):
+    """C1 (256 curves) through the default choice (the 4-lane latency kernel at this size) and
+    both kernels forced: every output bit-exact."""
     cfg = ecm_config("C1")
     k, _ = orc.stage1_k(cfg["B1"])
-    got = gpu_stage1(torch, cfg["N"], cfg["L"], cfg["B1"], cfg["sigmas"])
+    got = gpu_stage1(torch, cfg["N"], cfg["L"], cfg["B1"], cfg["sigmas"], flags=KERNELS[kernel])
     want = orc.ecm_stage1_mt(cfg["N"], cfg["L"], k, cfg["sigmas"])
     assert_same(got, want)
     found = got["status"] == 1
@@ -47,20 +53,22 @@ def test_c1_all_curves_bit_exact(orc, torch):
         assert eg.limbs_to_int(row) == cfg["p"]
 
 
+@pytest.mark.parametrize("kernel", ["lanes1", "lanes4"])
 @pytest.mark.parametrize("L,nbits,pbits", [(4, 126, 30), (6, 190, 40), (8, 254, 40), (12, 382, 40)])
-def test_widths_ragged_counts(orc, torch, L, nbits, pbits):
+def test_widths_ragged_counts(orc, torch, L, nbits, pbits, kernel):
     cfg = ecm_config(L=L, nbits=nbits, pbits=pbits, B1=400, curves=77, seed=20 + L)
     k, _ = orc.stage1_k(cfg["B1"])
-    got = gpu_stage1(torch, cfg["N"], L, cfg["B1"], cfg["sigmas"])
+    got = gpu_stage1(torch, cfg["N"], L, cfg["B1"], cfg["sigmas"], flags=KERNELS[kernel])
     want = orc.ecm_stage1_mt(cfg["N"], L, k, cfg["sigmas"])
     assert_same(got, want)
 
 
-def test_ladder_explicit_scalars(orc, torch):
+@pytest.mark.parametrize("kernel", ["lanes1", "lanes4"])
+def test_ladder_explicit_scalars(orc, torch, kernel):
     cfg = ecm_config(L=6, nbits=190, pbits=32, B1=100, curves=40, seed=31)
     s = torch.from_numpy(cfg["sigmas"]).cuda()
     for k in (1, 2, 3, 4, 5, 7, 0x1F3, (1 << 200) + 12345, 2520):
-        r = eg.ecm_ladder_batch(cfg["N"], 6, k, s)
+        r = eg.ecm_ladder_batch(cfg["N"], 6, k, s, flags=KERNELS[kernel])
         got = {kk: v.cpu().numpy() for kk, v in r.items()}
         want = orc.ecm_stage1(cfg["N"], 6, k, cfg["sigmas"])
         assert_same(got, want)
