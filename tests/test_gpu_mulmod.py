@@ -221,3 +221,55 @@ def test_stream_kernel_in_place(orc, torch):
         eg.ecm_mulmod_batch(A, B, Nn, A, L=L, iters=2, flags=fl | eg.ECM_KERNEL_STREAM)
         got = A.cpu().numpy()
         assert np.array_equal(got.T if tr else got, want), fl
+
+
+def _random_triples_on_device(torch, count, L, sliced, seed):
+    """Valid (a, b, n) limb arrays generated on the device (too large to build on the host):
+    n odd with bitlen exactly 32L-2, a, b < n (top limb reduced below n's).  Returned as flat
+    uint32-sized tensors in the requested layout, plus a (count, L) / (L, count) view helper."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    shape = (L, count) if sliced else (count, L)
+    arrs = [torch.randint(0, 256, (count * L * 4,), dtype=torch.uint8, device="cuda", generator=g)
+            .view(torch.int32).view(*shape) for _ in range(3)]
+    a, b, n = arrs
+    top = (lambda t: t[L - 1]) if sliced else (lambda t: t[:, L - 1])
+    low = (lambda t: t[0]) if sliced else (lambda t: t[:, 0])
+    low(n).bitwise_or_(1)
+    nt = top(n)
+    nt.bitwise_and_((1 << 29) - 1).bitwise_or_(1 << 29)  # bitlen(n) = 32L - 2
+    for x in (a, b):
+        xt = top(x)
+        xt.copy_(torch.remainder(xt, nt))  # top limb < n's -> x < n
+    return a, b, n
+
+
+@pytest.mark.parametrize("layout", ("aos", "sliced"))
+def test_max_size_64bit_offsets(orc, torch, layout):
+    """Maximum sizes: count = 2^30 + 5 triples at L = 6 (24 GiB per array; word offsets up to
+    6.4e9 > 2^32 in both layouts), the streaming kernel (K = 1) and the warp-tile kernel (K = 8),
+    checked on a sample that includes the ragged tail and the last elements."""
+    L, count = 6, (1 << 30) + 5
+    free, _ = torch.cuda.mem_get_info()
+    if free < 4 * count * L * 4 + (8 << 30):
+        pytest.skip(f"needs ~{4 * count * L * 4 >> 30} GiB of free device memory")
+    sliced = layout == "sliced"
+    a, b, n = _random_triples_on_device(torch, count, L, sliced, seed=7)
+    out = torch.empty_like(a)
+    flags = eg.ECM_LAYOUT_SLICED if sliced else 0
+    idx = np.unique(np.concatenate([np.linspace(0, count - 1, 3000).astype(np.int64),
+                                    np.arange(count - 300, count), np.arange(0, 64),
+                                    [(1 << 32) // L - 1, (1 << 32) // L, (1 << 32) // L + 1]]))
+    it = torch.from_numpy(idx).cuda()
+
+    def rows(t):  # (len(idx), L) host copies of the sampled elements
+        r = t[:, it].t() if sliced else t[it]
+        return r.contiguous().cpu().numpy().view(np.uint32)
+
+    ah, bh, nh = rows(a), rows(b), rows(n)
+    for iters in (1, 8):
+        eg.ecm_mulmod_batch(a, b, n, out, L=L, iters=iters, flags=flags)
+        torch.cuda.synchronize()
+        want = orc.mulmod_chain_mt(ah, bh, nh, L, iters)
+        assert np.array_equal(rows(out), want), iters
+    del a, b, n, out
+    torch.cuda.empty_cache()
