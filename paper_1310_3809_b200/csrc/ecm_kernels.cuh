@@ -34,6 +34,10 @@ constexpr int kEcmTPB = 128;
 #ifndef ECM_SWAP_BRANCH
 #define ECM_SWAP_BRANCH 0
 #endif
+//   ECM_CONST_SMEM  : 1 = x0 and a24 live in shared memory during the ladder (loaded per use)
+#ifndef ECM_CONST_SMEM
+#define ECM_CONST_SMEM 0
+#endif
 // The default L <= 6 ladder is held to 80 registers = 6 CTAs x 4 warps per SM (at 81..88 the
 // 256-register warp allocation granule leaves 5); the cap costs one spill load per step.
 __host__ __device__ constexpr int ecm_min_blocks(int L, int V, bool eager, bool primes) {
@@ -223,6 +227,45 @@ __device__ __forceinline__ void ladder_step(uint32_t (&X0)[L], uint32_t (&Z0)[L]
   f.sqr(X1, t3);
   f.sqr(t4, t4);
   f.mul(Z1, x0, t4);
+}
+
+// ECM_CONST_SMEM: the step with x0 and a24 read from shared memory ([word][thread], conflict-free)
+// right before their products, so they are not live in registers across the step.
+__device__ __forceinline__ uint32_t lds_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+  return v;
+}
+template <int L, int TPB>
+__device__ __forceinline__ void lds_res(uint32_t (&d)[L], const uint32_t* base) {
+#pragma unroll
+  for (int k = 0; k < L; ++k) d[k] = lds_u32(base + k * TPB);
+}
+template <int L, int TPB, class F>
+__device__ __forceinline__ void ladder_step_sm(uint32_t (&X0)[L], uint32_t (&Z0)[L], uint32_t (&X1)[L],
+                                               uint32_t (&Z1)[L], const uint32_t* sx0, const uint32_t* sa24,
+                                               const F& f) {
+  uint32_t t1[L], t2[L], t3[L], t4[L], U[L], V[L], s[L], d[L], c[L];
+  f.add(t1, X0, Z0);
+  f.sub(t2, X0, Z0);
+  f.add(t3, X1, Z1);
+  f.sub(t4, X1, Z1);
+  f.mul(U, t2, t3);
+  f.mul(V, t1, t4);
+  f.sqr(s, t1);
+  f.sqr(d, t2);
+  f.mul(X0, s, d);
+  f.sub(t1, s, d);
+  lds_res<L, TPB>(c, sa24);
+  f.mul(t2, c, t1);
+  f.add(t2, d, t2);
+  f.mul(Z0, t1, t2);
+  f.add(t3, U, V);
+  f.sub(t4, U, V);
+  f.sqr(X1, t3);
+  f.sqr(t4, t4);
+  lds_res<L, TPB>(c, sx0);
+  f.mul(Z1, c, t4);
 }
 
 // The same step with a projective difference D = (Xd:Zd) (the paper-comparable prime-by-prime
@@ -446,6 +489,11 @@ __global__ void __launch_bounds__(kEcmTPB, ecm_min_blocks(L, VAR, EAGER, PRIMES)
   copy(X0, x0);
   copy(Z0, ONE);
   if (!PRIMES) xdbl<L>(X1, Z1, X0, Z0, a24, fld);  // R1 = xDBL(P)
+#if ECM_CONST_SMEM
+  __shared__ uint32_t sm_c[2][L][kEcmTPB];
+#pragma unroll
+  for (int k = 0; k < L; ++k) { sm_c[0][k][threadIdx.x] = x0[k]; sm_c[1][k][threadIdx.x] = a24[k]; }
+#endif
   if (!PRIMES) {
     bool swapped = false;
     if (k_bits >= 2) {
@@ -470,7 +518,11 @@ __global__ void __launch_bounds__(kEcmTPB, ecm_min_blocks(L, VAR, EAGER, PRIMES)
         cswap<L>(X0, X1, bit != swapped);
         cswap<L>(Z0, Z1, bit != swapped);
         swapped = bit;
+#if ECM_CONST_SMEM
+        ladder_step_sm<L, kEcmTPB>(X0, Z0, X1, Z1, &sm_c[0][0][threadIdx.x], &sm_c[1][0][threadIdx.x], fld);
+#else
         ladder_step<L>(X0, Z0, X1, Z1, x0, a24, fld);
+#endif
 #endif
       }
     }
