@@ -335,6 +335,25 @@ def run_ours(args):
                             "frac": curves_s / ws * fpe_curve / pk["fpe_peak"]},
                "clocks": clk2.summary()}
 
+    # ---------------- ECM width sweep (C4's widths for stage 1): 2^17 curves per width ----------------
+    if ecm is not None and not args.no_sweep:
+        ecm["widths"] = {}
+        for Lw in (4, 6, 8, 12, 16):
+            cw = ecm_config(L=Lw, nbits=32 * Lw - 2, pbits=64, B1=cfg["B1"], curves=args.ecm_width_curves,
+                            seed=40 + Lw)
+            sw = torch.from_numpy(cw["sigmas"][rank::ws].copy()).cuda()
+            eg.ecm_stage1_batch(cw["N"], Lw, cw["B1"], sw[:1024], want=("g",))
+            rw = {}
+            msw, _ = time_steps(torch, lambda: rw.update(eg.ecm_stage1_batch(cw["N"], Lw, cw["B1"], sw, want=("g",))),
+                                1, ws)
+            msw = max_over_ranks(torch, msw, ws)
+            cps = args.ecm_width_curves / (msw * 1e-3)
+            fpe_w = (kb - 1) * (18 * Lw * Lw + 2 * Lw)
+            ecm["widths"][f"L{Lw}"] = {"bits": 32 * Lw - 2, "curves": args.ecm_width_curves, "ms": msw,
+                                       "curves_per_s": cps, "modmul_per_s": cps * (kb - 1) * MULMODS_PER_STEP,
+                                       "frac": cps / ws * fpe_w / pk["fpe_peak"]}
+            del sw
+
     # ---------------- C1: 256 curves, B1 = 2000 — latency bound (report time, not roofline) --------
     c1 = None
     if not args.no_ecm:
@@ -461,6 +480,7 @@ def main():
     ap.add_argument("--iters", type=int, default=C2_ITERS)
     ap.add_argument("--no-ecm", action="store_true")
     ap.add_argument("--ecm-curves", type=int, default=None)
+    ap.add_argument("--ecm-width-curves", type=int, default=1 << 17, help="curves per width in the ECM width sweep")
     ap.add_argument("--ecm-b1", type=int, default=None, help="override C3's B1 (tests / profiling only)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")

@@ -13,8 +13,8 @@
  *
  * Conventions (all entry points)
  *   - Integers are little-endian arrays of uint32 limbs; L limbs per integer: L in {4,6,8,12,16}
- *     for ecm_mulmod_batch, L in {4,6,8,12} for the ECM entry points ("b-bit" = 32L bits of
- *     storage, moduli of at most 32L-2 bits: PAPER.md:189; 510-bit moduli at L = 16).
+ *     for every entry point ("b-bit" = 32L bits of storage, moduli of at most 32L-2 bits:
+ *     PAPER.md:189; 510-bit moduli at L = 16, "510 bit arithmetic should work").
  *     R = 2^(32L).
  *   - Arrays of `count` integers are AoS by default: element i occupies words [i*L, i*L+L).
  *     With ECM_LAYOUT_SLICED (mulmod only) limb j of element i is at word [j*count + i].

@@ -29,10 +29,10 @@ constexpr uint32_t kKnownFlags = ECM_CANONICAL | ECM_SQUARE | ECM_LAYOUT_SLICED 
                                  ECM_NO_XAFF | ECM_EAGER | ECM_PRIME_LADDERS | ECM_REDC_MASK |
                                  ECM_KERNEL_STREAM | ECM_KERNEL_WARP | ECM_KERNEL_LANES4 | ECM_KERNEL_LANES1;
 
-// widths: mulmod L in {4, 6, 8, 12, 16}; ECM L in {4, 6, 8, 12} (at L = 16 the six-residue ladder
-// state does not fit the register file without splitting a curve across threads, §8(f) N3)
-bool valid_L(int L) { return L == 4 || L == 6 || L == 8 || L == 12; }
-bool valid_L_mulmod(int L) { return valid_L(L) || L == 16; }
+// widths: L in {4, 6, 8, 12, 16} for mulmod and ECM (510-bit moduli at L = 16; the
+// L = 16 ladder kernel holds its six-residue state in 254 registers without spilling)
+bool valid_L(int L) { return L == 4 || L == 6 || L == 8 || L == 12 || L == 16; }
+bool valid_L_mulmod(int L) { return valid_L(L); }
 
 // ---- host multiprecision helpers (little-endian 32-bit words, fixed width W) ----
 int bitlen(const uint32_t* a, int W) {

@@ -21,6 +21,7 @@ cudaError_t launch_ecm(const EcmParams& p, const uint32_t* kw, uint32_t k_bits, 
     case 6: return launch_ecm_L<6>(p, kw, k_bits, sigmas, count, X, Z, g, status, xaff, flags, s);
     case 8: return launch_ecm_L<8>(p, kw, k_bits, sigmas, count, X, Z, g, status, xaff, flags, s);
     case 12: return launch_ecm_L<12>(p, kw, k_bits, sigmas, count, X, Z, g, status, xaff, flags, s);
+    case 16: return launch_ecm_L<16>(p, kw, k_bits, sigmas, count, X, Z, g, status, xaff, flags, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -78,8 +78,11 @@ def test_argument_errors_before_any_device_work(L):
     assert lib.ecm_stage1_batch(Np, 7, 100, sp, 4, None, None, None, stp, None, 0, None) == 1
     N16 = np.zeros(16, np.uint32)
     N16[0] = 11
+    assert lib.ecm_stage1_batch(N16.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), 10, 100, sp, 4,
+                                None, None, None, stp, None, 0, None) == 1  # no L = 10
+    # ablation variants exist for L = 6, 8 only
     assert lib.ecm_stage1_batch(N16.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)), 16, 100, sp, 4,
-                                None, None, None, stp, None, 0, None) == 1  # no ECM at L = 16
+                                None, None, None, stp, None, 0x40, None) == 1
     # stage-1 kernel choice: not both; the 4-lane kernel only for the default lazy full-k ladder;
     # not a mulmod flag
     assert lib.ecm_stage1_batch(Np, 6, 100, sp, 4, None, None, None, stp, None, 0x6000, None) == 1

@@ -54,7 +54,7 @@ def test_c1_all_curves_bit_exact(orc, torch, kernel):
 
 
 @pytest.mark.parametrize("kernel", ["lanes1", "lanes4"])
-@pytest.mark.parametrize("L,nbits,pbits", [(4, 126, 30), (6, 190, 40), (8, 254, 40), (12, 382, 40)])
+@pytest.mark.parametrize("L,nbits,pbits", [(4, 126, 30), (6, 190, 40), (8, 254, 40), (12, 382, 40), (16, 510, 40)])
 def test_widths_ragged_counts(orc, torch, L, nbits, pbits, kernel):
     cfg = ecm_config(L=L, nbits=nbits, pbits=pbits, B1=400, curves=77, seed=20 + L)
     k, _ = orc.stage1_k(cfg["B1"])
