@@ -229,31 +229,39 @@ ecm_status run_ecm(const uint32_t* N_host, int L, const uint32_t* kw_dev, uint32
 }
 
 // ECM_HOST_BUFFERS without ECM_CHECK (AoS or limb-sliced): the batch is cut into chunks that cycle
-// through two internal streams, so the host->device copy of chunk c+1, the kernel of chunk c and
-// the device->host copy of chunk c-1 overlap (copy engines and SMs run concurrently).
+// through three internal streams, so the host->device copy of chunk c+1, the kernel of chunk c and
+// the device->host copy of chunk c-1 overlap (copy engines and SMs run concurrently).  Chunks are
+// whole waves of the kernel that runs them (SMs x resident CTAs x elements per CTA), so no chunk
+// ends in a partly filled wave; the first chunk is one wave, so the pipeline fills in one small
+// copy, and the rest are about count/32 elements each.
+constexpr int kPipeStreams = 3;
 cudaError_t mulmod_host_pipelined(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out,
                                   size_t count, int L, uint32_t iters, uint32_t flags, cudaStream_t s) {
   const bool square = flags & ECM_SQUARE;
   const bool sliced = flags & ECM_LAYOUT_SLICED;
-  size_t chunk = (count + 7) / 8;
-  if (chunk < ((size_t)1 << 18)) chunk = (size_t)1 << 18;
-  chunk = (chunk + 31) / 32 * 32;
+  size_t wave = 0;
+  cudaError_t e = ecm::launch_mulmod(nullptr, nullptr, nullptr, nullptr, (size_t)1 << 24, L, iters, flags, s, &wave);
+  if (e != cudaSuccess) return e;
+  if (wave == 0) wave = 1u << 16;
+  size_t chunk = (count / 32 + wave - 1) / wave * wave;
+  if (chunk < wave) chunk = wave;
   const size_t cw = chunk * (size_t)L;  // words per array per slot
   uint32_t* scratch = nullptr;
-  cudaError_t e = dev_alloc(&scratch, 2 * 4 * cw * sizeof(uint32_t), s);
+  e = dev_alloc(&scratch, kPipeStreams * 4 * cw * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
-  cudaStream_t st[2] = {nullptr, nullptr};
-  cudaEvent_t start = nullptr, done[2] = {nullptr, nullptr};
-  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking);
+  cudaStream_t st[kPipeStreams] = {};
+  cudaEvent_t start = nullptr, done[kPipeStreams] = {};
+  for (int i = 0; i < kPipeStreams && e == cudaSuccess; ++i) e = cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
-  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
+  for (int i = 0; i < kPipeStreams && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventRecord(start, s);
-  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(st[i], start, 0);
-  for (size_t c0 = 0, c = 0; c0 < count && e == cudaSuccess; c0 += chunk, ++c) {
-    const size_t m = (count - c0) < chunk ? (count - c0) : chunk;
+  for (int i = 0; i < kPipeStreams && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(st[i], start, 0);
+  for (size_t c0 = 0, c = 0; c0 < count && e == cudaSuccess; ++c) {
+    const size_t want = c == 0 ? wave : chunk;
+    const size_t m = (count - c0) < want ? (count - c0) : want;
     const size_t by = m * (size_t)L * sizeof(uint32_t);
-    cudaStream_t q = st[c & 1];
-    uint32_t* base = scratch + (c & 1) * 4 * cw;
+    cudaStream_t q = st[c % kPipeStreams];
+    uint32_t* base = scratch + (c % kPipeStreams) * 4 * cw;
     uint32_t *ta = base, *tb = base + cw, *tn = base + 2 * cw, *to = base + 3 * cw;
     if (!sliced) {
       e = cudaMemcpyAsync(ta, a + c0 * L, by, cudaMemcpyHostToDevice, q);
@@ -275,8 +283,9 @@ cudaError_t mulmod_host_pipelined(const uint32_t* a, const uint32_t* b, const ui
         e = cudaMemcpy2DAsync(out + c0, count * sizeof(uint32_t), to, m * sizeof(uint32_t), m * sizeof(uint32_t), L,
                               cudaMemcpyDeviceToHost, q);
     }
+    c0 += m;
   }
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kPipeStreams; ++i) {
     if (done[i] && st[i]) {
       cudaEventRecord(done[i], st[i]);
       cudaStreamWaitEvent(s, done[i], 0);
@@ -284,7 +293,7 @@ cudaError_t mulmod_host_pipelined(const uint32_t* a, const uint32_t* b, const ui
   }
   cudaFreeAsync(scratch, s);
   const cudaError_t e2 = cudaStreamSynchronize(s);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kPipeStreams; ++i) {
     if (st[i]) cudaStreamDestroy(st[i]);
     if (done[i]) cudaEventDestroy(done[i]);
   }

@@ -38,10 +38,15 @@ constexpr int kEcmTPB = 128;
 #ifndef ECM_CONST_SMEM
 #define ECM_CONST_SMEM 0
 #endif
-// The default L <= 6 ladder is held to 80 registers = 6 CTAs x 4 warps per SM (at 81..88 the
-// 256-register warp allocation granule leaves 5); the cap costs one spill load per step.
+// Occupancy of the default ladder (tools/ecm_ab.py, profiles/r01_ecm_ab.jsonl): L <= 6 is held to
+// 80 registers = 6 CTAs x 4 warps per SM (at 81..88 the 256-register warp allocation granule leaves
+// 5; the cap costs one spill load per step); L = 12 to 168 = 3 CTAs (+6 % over 182 registers and 2
+// CTAs, no spills).  L = 8 (138 registers, 3 CTAs) measured the same at 4 CTAs; L = 4 and 16 are
+// left to ptxas.
 __host__ __device__ constexpr int ecm_min_blocks(int L, int V, bool eager, bool primes) {
-  return ECM_MIN_BLOCKS >= 0 ? ECM_MIN_BLOCKS : (L <= 6 && V == 0 && !eager && !primes) ? 6 : 0;
+  return ECM_MIN_BLOCKS >= 0 ? ECM_MIN_BLOCKS
+         : (V != 0 || eager || primes) ? 0
+         : L <= 6 ? 6 : L == 12 ? 3 : 0;
 }
 
 template <int L>

@@ -7,14 +7,15 @@
 
 namespace ecm {
 
+// wave != nullptr: launch nothing; *wave = elements per full wave of the kernel the call would run
 cudaError_t launch_mulmod(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out, size_t count,
-                          int L, uint32_t iters, uint32_t flags, cudaStream_t s);
+                          int L, uint32_t iters, uint32_t flags, cudaStream_t s, size_t* wave = nullptr);
 cudaError_t launch_mulmod_check(const uint32_t* a, const uint32_t* b, const uint32_t* n, size_t count, int L,
                                 uint32_t flags, uint32_t* err, cudaStream_t s);
 
-// ECM stage 1: N, 2N, n0inv, R^2 mod N and the scalar bits (MSB first) are uploaded by the
-// host into a per-call parameter block (struct below), then three kernels run:
-//   setup (Suyama + inverse), ladder (hot loop), tail (gcd, affine x, canonical X, Z).
+// ECM stage 1: N, 2N, n0inv, R^2 mod N, R mod N and -N^{-1} mod R go to the kernel as a parameter
+// block (struct below, constant bank); the scalar plan (bits of k, or the prime list) is a device
+// buffer.  One kernel per call runs setup, ladder and tail (ecm_kernels.cuh).
 struct EcmParams {
   int L;
   uint32_t n0inv;

@@ -10,7 +10,7 @@ namespace ecm {
 
 template <int L>
 cudaError_t launch_mulmod_L(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out, size_t count,
-                            uint32_t iters, uint32_t flags, cudaStream_t s);
+                            uint32_t iters, uint32_t flags, cudaStream_t s, size_t* wave);
 
 // ---- precondition check (ECM_CHECK): n odd, bitlen(n) <= 32L-2, a, b < 2n ----
 template <int L>
@@ -52,13 +52,13 @@ __global__ void mulmod_check_kernel(const uint32_t* __restrict__ a, const uint32
 }
 
 cudaError_t launch_mulmod(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out, size_t count,
-                          int L, uint32_t iters, uint32_t flags, cudaStream_t s) {
+                          int L, uint32_t iters, uint32_t flags, cudaStream_t s, size_t* wave) {
   switch (L) {
-    case 6: return launch_mulmod_L<6>(a, b, n, out, count, iters, flags, s);
-    case 4: return launch_mulmod_L<4>(a, b, n, out, count, iters, flags, s);
-    case 8: return launch_mulmod_L<8>(a, b, n, out, count, iters, flags, s);
-    case 12: return launch_mulmod_L<12>(a, b, n, out, count, iters, flags, s);
-    case 16: return launch_mulmod_L<16>(a, b, n, out, count, iters, flags, s);
+    case 6: return launch_mulmod_L<6>(a, b, n, out, count, iters, flags, s, wave);
+    case 4: return launch_mulmod_L<4>(a, b, n, out, count, iters, flags, s, wave);
+    case 8: return launch_mulmod_L<8>(a, b, n, out, count, iters, flags, s, wave);
+    case 12: return launch_mulmod_L<12>(a, b, n, out, count, iters, flags, s, wave);
+    case 16: return launch_mulmod_L<16>(a, b, n, out, count, iters, flags, s, wave);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -430,9 +430,11 @@ static inline cudaError_t stream_occupancy(const void* kern, size_t smem, int* o
   return cudaSuccess;
 }
 
+// wave != nullptr: launch nothing, return in *wave the elements one full wave of the kernel this
+// call would run processes (SMs x resident CTAs x elements per CTA), for wave-multiple chunking.
 template <int L, int V>
 static cudaError_t launch_mulmod_LV(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out,
-                                    size_t count, uint32_t iters, uint32_t flags, cudaStream_t s) {
+                                    size_t count, uint32_t iters, uint32_t flags, cudaStream_t s, size_t* wave) {
   const size_t ntiles = (count + 31) / 32;
   size_t blocks = (ntiles + (kMulmodTPB / 32) - 1) / (kMulmodTPB / 32);
   if (blocks > 0x7fffffffull) blocks = 0x7fffffffull;
@@ -440,10 +442,23 @@ static cudaError_t launch_mulmod_LV(const uint32_t* a, const uint32_t* b, const 
   const bool sq = flags & 0x2u, sl = flags & 0x4u;
   constexpr size_t smem = (size_t)(kMulmodTPB / 32) * (3 * 32 * L * sizeof(uint32_t) + sizeof(uint64_t));
   static_assert(smem <= 200 * 1024, "tile staging does not fit shared memory");
+  auto sm_count = [](int* sms) -> cudaError_t {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev);
+    return e;
+  };
   auto go = [&](auto kern) -> cudaError_t {
     if (smem > 48 * 1024) {
       const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
+    }
+    if (wave) {
+      int occ = 0, sms = 0;
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kMulmodTPB, smem);
+      if (e == cudaSuccess) e = sm_count(&sms);
+      *wave = (size_t)sms * (size_t)(occ > 0 ? occ : 1) * kMulmodTPB;
+      return e;
     }
     kern<<<g, kMulmodTPB, smem, s>>>(a, b, n, out, count, iters, flags);
     return cudaGetLastError();
@@ -454,12 +469,15 @@ static cudaError_t launch_mulmod_LV(const uint32_t* a, const uint32_t* b, const 
       int occ = 0;
       cudaError_t e = stream_occupancy(reinterpret_cast<const void*>(kern), ssm, &occ);
       if (e != cudaSuccess) return e;
-      int dev = 0, sms = 0;
-      e = cudaGetDevice(&dev);
-      if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      int sms = 0;
+      e = sm_count(&sms);
       if (e != cudaSuccess) return e;
       const size_t nfull = count / kStreamTPB;
       size_t grid = (size_t)sms * (size_t)(occ > 0 ? occ : 1);
+      if (wave) {
+        *wave = grid * kStreamTPB;
+        return cudaSuccess;
+      }
       if (grid > nfull) grid = nfull > 0 ? nfull : 1;
       kern<<<(unsigned)grid, kStreamTPB, ssm, s>>>(a, b, n, out, count, iters, flags);
       return cudaGetLastError();
@@ -477,13 +495,13 @@ static cudaError_t launch_mulmod_LV(const uint32_t* a, const uint32_t* b, const 
 
 template <int L>
 cudaError_t launch_mulmod_L(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out,
-                                   size_t count, uint32_t iters, uint32_t flags, cudaStream_t s) {
+                                   size_t count, uint32_t iters, uint32_t flags, cudaStream_t s, size_t* wave) {
   switch ((flags >> 8) & 7u) {
-    case REDC_WORD: return launch_mulmod_LV<L, REDC_WORD>(a, b, n, out, count, iters, flags, s);
-    case REDC_KNOWNLOW: return launch_mulmod_LV<L, REDC_KNOWNLOW>(a, b, n, out, count, iters, flags, s);
-    case REDC_BLOCKTHM: return launch_mulmod_LV<L, REDC_BLOCKTHM>(a, b, n, out, count, iters, flags, s);
-    case REDC_CLASSIC: return launch_mulmod_LV<L, REDC_CLASSIC>(a, b, n, out, count, iters, flags, s);
-    case REDC_KARATSUBA: return launch_mulmod_LV<L, REDC_KARATSUBA>(a, b, n, out, count, iters, flags, s);
+    case REDC_WORD: return launch_mulmod_LV<L, REDC_WORD>(a, b, n, out, count, iters, flags, s, wave);
+    case REDC_KNOWNLOW: return launch_mulmod_LV<L, REDC_KNOWNLOW>(a, b, n, out, count, iters, flags, s, wave);
+    case REDC_BLOCKTHM: return launch_mulmod_LV<L, REDC_BLOCKTHM>(a, b, n, out, count, iters, flags, s, wave);
+    case REDC_CLASSIC: return launch_mulmod_LV<L, REDC_CLASSIC>(a, b, n, out, count, iters, flags, s, wave);
+    case REDC_KARATSUBA: return launch_mulmod_LV<L, REDC_KARATSUBA>(a, b, n, out, count, iters, flags, s, wave);
     default: return cudaErrorInvalidValue;
   }
 }

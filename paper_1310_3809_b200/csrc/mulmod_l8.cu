@@ -4,5 +4,5 @@
 
 namespace ecm {
 template cudaError_t launch_mulmod_L<8>(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out,
-                                 size_t count, uint32_t iters, uint32_t flags, cudaStream_t s);
+                                 size_t count, uint32_t iters, uint32_t flags, cudaStream_t s, size_t* wave);
 }  // namespace ecm

@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """A/B experiments on build-time variants of the ECM ladder kernel (ecm_kernels.cuh knobs).
 
-    python tools/ecm_ab.py build NAME "-DECM_SWAP_BRANCH=1 -DECM_MIN_BLOCKS=7" [NAME2 "FLAGS2" ...]
+    python tools/ecm_ab.py build [--L 6] NAME "-DECM_SWAP_BRANCH=1 -DECM_MIN_BLOCKS=7" [NAME2 "FLAGS2" ...]
         compiles csrc/ecm_l<L>.cu and mulmod_l<L>.cu with the flags and links it with the product objects of
         paper_1310_3809_b200/_build into tools/_variants/libecmgpu_NAME.so (here, on CPU)
     python tools/ecm_ab.py time [--curves 1048576,131072] [--B1 50000] [--L 6] NAME ...
@@ -59,7 +59,8 @@ def time_one(name, curves_list, B1, L):
         _lib.library_path = os.path.join(VAR, f"libecmgpu_{name}.so")
     import paper_1310_3809_b200 as eg
     from workload import ecm_config
-    cfg = ecm_config("C3") if L == 6 else ecm_config("C5")
+    cfg = ecm_config("C3") if L == 6 else ecm_config("C5") if L == 8 else \
+        ecm_config(L=L, nbits=32 * L - 2, pbits=64, B1=B1, curves=max(curves_list), seed=40 + L)
     if os.environ.get("AB_MULMOD", "1") == "1":
         from workload import mulmod_inputs
         a, b, n = (torch.from_numpy(v.T.copy()).cuda() for v in mulmod_inputs(1 << 24, L, seed=2))
@@ -98,7 +99,10 @@ def time_one(name, curves_list, B1, L):
 def main():
     if sys.argv[1] == "build":
         a = sys.argv[2:]
-        build(list(zip(a[0::2], a[1::2])))
+        L = 6
+        if a and a[0] == "--L":
+            L, a = int(a[1]), a[2:]
+        build(list(zip(a[0::2], a[1::2])), L=L)
     elif sys.argv[1] == "time":
         import argparse
         ap = argparse.ArgumentParser()
