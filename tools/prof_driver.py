@@ -21,6 +21,7 @@ ap.add_argument("--curves", type=int, default=1 << 16)
 ap.add_argument("--B1", type=int, default=50000)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--sliced", action="store_true", help="limb-sliced layout (the bench headline)")
+ap.add_argument("--cfg", default="C3", help="ECM config for the modulus and seeds (C1, C3)")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 if a.what == "mulmod":
@@ -29,7 +30,7 @@ if a.what == "mulmod":
     for _ in range(a.reps):
         eg.ecm_mulmod_batch(x, y, n, L=a.L, iters=a.iters, flags=fl)
 else:
-    cfg = ecm_config("C3")
+    cfg = ecm_config(a.cfg)
     s = torch.from_numpy(cfg["sigmas"][: a.curves].copy()).cuda()
     for _ in range(a.reps):
         eg.ecm_stage1_batch(cfg["N"], 6, a.B1, s, want=("g",))

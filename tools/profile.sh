@@ -25,5 +25,6 @@ cap sqr mulmod_batch_kernel mulmod --sliced --flags 2 --reps 1
 cap k1 mulmod_ mulmod --iters 1 --reps 1
 cap k1_sliced mulmod_ mulmod --sliced --iters 1 --reps 1
 cap ecm ecm_stage1_kernel ecm --curves 1048576 --B1 2000 --reps 1
+cap ecm_c1 ecm_stage1_coop ecm --cfg C1 --curves 256 --B1 2000 --reps 1
 fi
 ls -la $OUT
