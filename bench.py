@@ -335,6 +335,25 @@ def run_ours(args):
                             "frac": curves_s / ws * fpe_curve / pk["fpe_peak"]},
                "clocks": clk2.summary()}
 
+    # ---------------- §8(f) N4: the small-parameter family on C3's modulus, B1 and curve count ----------
+    if ecm is not None and not args.no_sweep:
+        seeds_np = (cfg["sigmas"][:curves] % np.uint64((1 << 30) - 1)) + np.uint64(1)
+        sd = torch.from_numpy(seeds_np[lo:hi].copy()).cuda()
+        eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], sd[:4096], flags=eg.ECM_CURVE_SMALL, want=("g",))
+        rs = {}
+        mss, _ = time_steps(torch, lambda: rs.update(eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], sd,
+                                                                            flags=eg.ECM_CURVE_SMALL, want=("g",))),
+                            1, ws)
+        mss = max_over_ranks(torch, mss, ws)
+        cps = curves / (mss * 1e-3)
+        fpe_small = 4 * FPE_MUL + 4 * (3 * L * L + L) // 2 + 2 * L  # 4M + 4S + one word-level REDC
+        ecm["small_family"] = {"workload": "C3 modulus/B1/curves, a24 = s/2^32, x0 = 2 (SURVEY §8(f) N4; not the "
+                                           "paper's curves)", "curves_per_s": cps, "ms": mss,
+                               "flagged_factor_rank0": int((rs["status"] == 1).sum().item()),
+                               "speedup_vs_suyama": cps / curves_s,
+                               "frac": cps / ws * (kb - 1) * fpe_small / pk["fpe_peak"]}
+        del sd
+
     # ---------------- ECM width sweep (C4's widths for stage 1): 2^17 curves per width ----------------
     if ecm is not None and not args.no_sweep:
         ecm["widths"] = {}

@@ -88,6 +88,13 @@ typedef enum {
    lazy full-k ladder (ECM_E_ARG with ECM_EAGER, ECM_PRIME_LADDERS or another REDC variant). */
 #define ECM_KERNEL_LANES4 0x2000u
 #define ECM_KERNEL_LANES1 0x4000u
+/* stage 1 curve family (NOT the paper's curves, reading G16): seed s_i
+   in [1, 2^30) (passed in `sigmas`) selects B y^2 = x^3 + A x^2 + x with a24 = (A+2)/4 = s_i / 2^32
+   mod N and base point x0 = 2, so a24*t is one word-level REDC and x0*t an addition (8 instead of
+   10 full products per ladder step).  No setup inversion; a seed outside [1, 2^30) gives status
+   ECM_CURVE_BAD_SIGMA with g = N.  Default lazy full-k ladder only (ECM_E_ARG with ECM_EAGER,
+   ECM_PRIME_LADDERS or another REDC variant). */
+#define ECM_CURVE_SMALL 0x8000u
 
 /* Status values written per curve by ecm_stage1_batch / ecm_ladder_batch. */
 #define ECM_CURVE_NO_FACTOR 0    /* g == 1 */

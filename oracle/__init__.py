@@ -57,6 +57,8 @@ def lib():
         L.orc_ecm_stage1.argtypes = [_u32p, ctypes.c_int, _u32p, ctypes.c_uint32, _u64p, ctypes.c_size_t,
                                      _u32p, _u32p, _u32p, _u8p, _u32p]
         L.orc_ecm_stage1.restype = ctypes.c_int
+        L.orc_ecm_stage1_small.argtypes = L.orc_ecm_stage1.argtypes
+        L.orc_ecm_stage1_small.restype = ctypes.c_int
         L.orc_ecm_stage1_primes.argtypes = [_u32p, ctypes.c_int, ctypes.c_uint64, _u64p, ctypes.c_size_t,
                                             _u32p, _u32p, _u32p, _u8p, _u32p]
         L.orc_ecm_stage1_primes.restype = ctypes.c_int
@@ -161,8 +163,9 @@ def k_words(k: int) -> tuple[np.ndarray, int]:
     return to_limbs(k, nw), bits
 
 
-def ecm_stage1(N: int, L: int, k: int, sigmas, want_xaff: bool = True):
-    """Returns dict of numpy arrays X, Z, g (count, L), status (count,), xaff (count, L)."""
+def ecm_stage1(N: int, L: int, k: int, sigmas, want_xaff: bool = True, family: str = "suyama"):
+    """Returns dict of numpy arrays X, Z, g (count, L), status (count,), xaff (count, L).
+    family "suyama" (the paper's curves) or "small" (§8(f) N4: a24 = s/2^32, x0 = 2)."""
     sig = np.ascontiguousarray(np.asarray(sigmas, dtype=np.uint64))
     count = sig.size
     kw, kb = k_words(k)
@@ -172,8 +175,9 @@ def ecm_stage1(N: int, L: int, k: int, sigmas, want_xaff: bool = True):
     g = np.zeros((count, L), np.uint32)
     st = np.zeros(count, np.uint8)
     xa = np.zeros((count, L), np.uint32)
-    rc = lib().orc_ecm_stage1(_p(Nl), L, _p(kw), kb, _p(sig, _u64p), count, _p(X), _p(Z), _p(g),
-                              _p(st, _u8p), _p(xa) if want_xaff else None)
+    fn = {"suyama": lib().orc_ecm_stage1, "small": lib().orc_ecm_stage1_small}[family]
+    rc = fn(_p(Nl), L, _p(kw), kb, _p(sig, _u64p), count, _p(X), _p(Z), _p(g),
+            _p(st, _u8p), _p(xa) if want_xaff else None)
     if rc != 0:
         raise ValueError("orc_ecm_stage1: bad arguments")
     return {"X": X, "Z": Z, "g": g, "status": st, "xaff": xa}
@@ -245,11 +249,11 @@ def ecm_stage1_primes_mt(N, L, B1, sigmas, threads=None):
     return {key: np.concatenate([p[key] for p in parts], axis=0) for key in parts[0]}
 
 
-def ecm_stage1_mt(N, L, k, sigmas, threads=None):
+def ecm_stage1_mt(N, L, k, sigmas, threads=None, family="suyama"):
     sig = np.asarray(sigmas, dtype=np.uint64)
     threads = threads or os.cpu_count() or 1
     count = sig.size
     step = max(1, -(-count // (threads * 2)))
     idx = [(s, min(count, s + step)) for s in range(0, count, step)]
-    parts = _pool_map(lambda r: ecm_stage1(N, L, k, sig[r[0]:r[1]]), idx, threads)
+    parts = _pool_map(lambda r: ecm_stage1(N, L, k, sig[r[0]:r[1]], family=family), idx, threads)
     return {key: np.concatenate([p[key] for p in parts], axis=0) for key in parts[0]}

@@ -517,6 +517,36 @@ static int check_args(const uint32_t *N, int L, const uint32_t *k_words, uint32_
   return 0;
 }
 
+/* One curve after its setup: ladder over k, tail, outputs written at index i. */
+static void stage1_curve(const ctx_t *c, const uint32_t *N, const uint32_t *k_words, uint32_t k_bits, int st,
+                         const uint32_t *x0m, const uint32_t *a24m, uint32_t *gg, size_t i, uint32_t *X,
+                         uint32_t *Z, uint32_t *g, uint8_t *status, uint32_t *xaff) {
+  int L = c->L;
+  uint32_t Xn[ORC_MAXL], Zn[ORC_MAXL], xa[ORC_MAXL];
+  zero(Xn, L); zero(Zn, L); zero(xa, L);
+  if (st == 0) {
+    pt_t R0;
+    ladder(c, x0m, a24m, k_words, k_bits, &R0, NULL);
+    from_mont(c, R0.X, Xn);
+    from_mont(c, R0.Z, Zn);
+    /* tail: the gcd of the final denominator gives the factor */
+    uint32_t zi[ORC_MAXL];
+    if (inv_gcd(Zn, c->n, L, gg, zi)) {
+      uint32_t xm[ORC_MAXL], zim[ORC_MAXL], pm[ORC_MAXL];
+      to_mont(c, Xn, xm);
+      to_mont(c, zi, zim);
+      mmul(c, xm, zim, pm);
+      from_mont(c, pm, xa);
+    }
+    st = classify(gg, N, L);
+  }
+  if (X) copy(X + i * (size_t)L, Xn, L);
+  if (Z) copy(Z + i * (size_t)L, Zn, L);
+  if (g) copy(g + i * (size_t)L, gg, L);
+  if (status) status[i] = (uint8_t)st;
+  if (xaff) copy(xaff + i * (size_t)L, xa, L);
+}
+
 int orc_ecm_stage1(const uint32_t *N, int L, const uint32_t *k_words, uint32_t k_bits,
                    const uint64_t *sigmas, size_t count, uint32_t *X, uint32_t *Z, uint32_t *g,
                    uint8_t *status, uint32_t *xaff) {
@@ -524,31 +554,42 @@ int orc_ecm_stage1(const uint32_t *N, int L, const uint32_t *k_words, uint32_t k
   ctx_t c;
   ctx_init(&c, N, L);
   for (size_t i = 0; i < count; ++i) {
-    uint32_t x0m[ORC_MAXL], a24m[ORC_MAXL], gg[ORC_MAXL], Xn[ORC_MAXL], Zn[ORC_MAXL], xa[ORC_MAXL];
+    uint32_t x0m[ORC_MAXL], a24m[ORC_MAXL], gg[ORC_MAXL];
     zero(gg, L); gg[0] = 1;
-    zero(Xn, L); zero(Zn, L); zero(xa, L);
     int st = suyama_mont(&c, sigmas[i], x0m, a24m, gg);
-    if (st == 0) {
-      pt_t R0;
-      ladder(&c, x0m, a24m, k_words, k_bits, &R0, NULL);
-      from_mont(&c, R0.X, Xn);
-      from_mont(&c, R0.Z, Zn);
-      /* tail: the gcd of the final denominator gives the factor */
-      uint32_t zi[ORC_MAXL];
-      if (inv_gcd(Zn, c.n, L, gg, zi)) {
-        uint32_t xm[ORC_MAXL], zim[ORC_MAXL], pm[ORC_MAXL];
-        to_mont(&c, Xn, xm);
-        to_mont(&c, zi, zim);
-        mmul(&c, xm, zim, pm);
-        from_mont(&c, pm, xa);
-      }
-      st = classify(gg, N, L);
-    }
-    if (X) copy(X + i * (size_t)L, Xn, L);
-    if (Z) copy(Z + i * (size_t)L, Zn, L);
-    if (g) copy(g + i * (size_t)L, gg, L);
-    if (status) status[i] = (uint8_t)st;
-    if (xaff) copy(xaff + i * (size_t)L, xa, L);
+    stage1_curve(&c, N, k_words, k_bits, st, x0m, a24m, gg, i, X, Z, g, status, xaff);
+  }
+  return 0;
+}
+
+/* Small-parameter family (reading G16 — not the paper's curves): for a seed
+ * s in [1, 2^30), the curve B y^2 = x^3 + A x^2 + x with a24 = (A+2)/4 = s / 2^32 mod N and the
+ * base point x0 = 2.  Out-of-range seeds get status 3 (no curve). */
+static int small_mont_setup(const ctx_t *c, uint64_t s, uint32_t *x0m, uint32_t *a24m) {
+  int L = c->L;
+  if (s < 1 || s >= ((uint64_t)1 << 30)) return 3;
+  uint32_t w[2] = {0u, 1u}, t[ORC_MAXL], inv[ORC_MAXL], g[ORC_MAXL], sm[ORC_MAXL], im[ORC_MAXL];
+  mod_n(w, 2, c->n, t, L);                     /* 2^32 mod N */
+  if (!inv_gcd(t, c->n, L, g, inv)) return 3;  /* N odd: never */
+  small_mont(c, s, sm);                        /* s R        */
+  to_mont(c, inv, im);                         /* 2^-32 R    */
+  mmul(c, sm, im, a24m);                       /* a24 R = s 2^-32 R */
+  small_mont(c, 2, x0m);                       /* x0 = 2     */
+  return 0;
+}
+
+int orc_ecm_stage1_small(const uint32_t *N, int L, const uint32_t *k_words, uint32_t k_bits,
+                         const uint64_t *seeds, size_t count, uint32_t *X, uint32_t *Z, uint32_t *g,
+                         uint8_t *status, uint32_t *xaff) {
+  if (check_args(N, L, k_words, k_bits)) return -1;
+  ctx_t c;
+  ctx_init(&c, N, L);
+  for (size_t i = 0; i < count; ++i) {
+    uint32_t x0m[ORC_MAXL], a24m[ORC_MAXL], gg[ORC_MAXL];
+    zero(gg, L); gg[0] = 1;
+    int st = small_mont_setup(&c, seeds[i], x0m, a24m);
+    if (st) copy(gg, N, L); /* no curve: g = N */
+    stage1_curve(&c, N, k_words, k_bits, st, x0m, a24m, gg, i, X, Z, g, status, xaff);
   }
   return 0;
 }

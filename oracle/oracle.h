@@ -75,6 +75,13 @@ int orc_ecm_stage1(const uint32_t *N, int L, const uint32_t *k_words, uint32_t k
 int orc_ecm_stage1_primes(const uint32_t *N, int L, uint64_t B1, const uint64_t *sigmas, size_t count,
                           uint32_t *X, uint32_t *Z, uint32_t *g, uint8_t *status, uint32_t *xaff);
 
+/* Stage 1 on the small-parameter family (reading G16 — not the paper's curve
+ * model): seed s in [1, 2^30) gives a24 = s / 2^32 mod N and x0 = 2; same ladder, tail and
+ * outputs as orc_ecm_stage1.  A seed outside [1, 2^30) gives status 3 with g = N. */
+int orc_ecm_stage1_small(const uint32_t *N, int L, const uint32_t *k_words, uint32_t k_bits,
+                         const uint64_t *seeds, size_t count, uint32_t *X, uint32_t *Z, uint32_t *g,
+                         uint8_t *status, uint32_t *xaff);
+
 /* Suyama setup only (reading G10): returns status 0/3/4; on 0 writes the
  * canonical normal-domain x0 = u^3/v^3 and a24 = (v-u)^3(3u+v)/(16u^3 v). */
 int orc_suyama(const uint32_t *N, int L, uint64_t sigma, uint32_t *x0, uint32_t *a24, uint32_t *g);

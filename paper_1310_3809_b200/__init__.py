@@ -23,7 +23,7 @@ from . import _lib
 from ._lib import (  # noqa: F401  (flag constants re-exported)
     ECM_CANONICAL, ECM_SQUARE, ECM_LAYOUT_SLICED, ECM_CHECK, ECM_HOST_BUFFERS, ECM_NO_XAFF, ECM_EAGER, ECM_PRIME_LADDERS,
     ECM_REDC_WORD, ECM_REDC_KNOWNLOW, ECM_REDC_BLOCKTHM, ECM_REDC_CLASSIC, ECM_REDC_KARATSUBA,
-    ECM_KERNEL_STREAM, ECM_KERNEL_WARP, ECM_KERNEL_LANES4, ECM_KERNEL_LANES1,
+    ECM_KERNEL_STREAM, ECM_KERNEL_WARP, ECM_KERNEL_LANES4, ECM_KERNEL_LANES1, ECM_CURVE_SMALL,
     EcmError, lib, library_path,
 )
 

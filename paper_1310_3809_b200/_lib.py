@@ -28,6 +28,7 @@ ECM_KERNEL_STREAM = 0x800
 ECM_KERNEL_WARP = 0x1000
 ECM_KERNEL_LANES4 = 0x2000
 ECM_KERNEL_LANES1 = 0x4000
+ECM_CURVE_SMALL = 0x8000
 
 # every symbol include/ecmgpu.h declares (checked by tests/test_abi.py)
 EXPORTS = ("ecm_mulmod_batch", "ecm_stage1_batch", "ecm_ladder_batch", "ecm_stage1_kbits",

@@ -27,7 +27,8 @@ using ecm::EcmParams;
 
 constexpr uint32_t kKnownFlags = ECM_CANONICAL | ECM_SQUARE | ECM_LAYOUT_SLICED | ECM_CHECK | ECM_HOST_BUFFERS |
                                  ECM_NO_XAFF | ECM_EAGER | ECM_PRIME_LADDERS | ECM_REDC_MASK |
-                                 ECM_KERNEL_STREAM | ECM_KERNEL_WARP | ECM_KERNEL_LANES4 | ECM_KERNEL_LANES1;
+                                 ECM_KERNEL_STREAM | ECM_KERNEL_WARP | ECM_KERNEL_LANES4 | ECM_KERNEL_LANES1 |
+                                 ECM_CURVE_SMALL;
 
 // widths: L in {4, 6, 8, 12, 16} for mulmod and ECM (510-bit moduli at L = 16; the
 // L = 16 ladder kernel holds its six-residue state in 254 registers without spilling)
@@ -148,6 +149,7 @@ bool ecm_variant_ok(int L, uint32_t flags) {
   const bool ablation = (flags & ECM_REDC_MASK) || (flags & ECM_EAGER);
   if ((flags & ECM_KERNEL_LANES4) && (flags & ECM_KERNEL_LANES1)) return false;
   if ((flags & ECM_KERNEL_LANES4) && (ablation || (flags & ECM_PRIME_LADDERS))) return false;
+  if ((flags & ECM_CURVE_SMALL) && (ablation || (flags & ECM_PRIME_LADDERS))) return false;
   if (flags & ECM_PRIME_LADDERS) {
     if (L == 8) return (flags & ECM_REDC_MASK) != ECM_REDC_KNOWNLOW;
     return L == 6 && !ablation;
@@ -334,7 +336,8 @@ ecm_status ecm_mulmod_batch(const uint32_t* a, const uint32_t* b, const uint32_t
   if (!a || !n || !out || (!b && !square) || count == 0 || !valid_L_mulmod(L) || iters == 0 ||
       (flags & ~kKnownFlags))
     return ECM_E_ARG;
-  if (flags & (ECM_NO_XAFF | ECM_EAGER | ECM_PRIME_LADDERS | ECM_KERNEL_LANES4 | ECM_KERNEL_LANES1)) return ECM_E_ARG;
+  if (flags & (ECM_NO_XAFF | ECM_EAGER | ECM_PRIME_LADDERS | ECM_KERNEL_LANES4 | ECM_KERNEL_LANES1 | ECM_CURVE_SMALL))
+    return ECM_E_ARG;
   if ((flags & ECM_REDC_MASK) > ECM_REDC_KARATSUBA) return ECM_E_ARG;
   if ((flags & ECM_KERNEL_STREAM) && (flags & ECM_KERNEL_WARP)) return ECM_E_ARG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -273,6 +273,33 @@ __device__ __forceinline__ void ladder_step_sm(uint32_t (&X0)[L], uint32_t (&Z0)
   f.mul(Z1, c, t4);
 }
 
+// The step on the small-parameter family (FAM 1): a24 t = c t / 2^32 by one word-level REDC
+// (mont_smul, 2L products) and x0 (U-V)^2 = 2 (U-V)^2 by a lazy addition — 8 full products per step.
+template <int L, class F>
+__device__ __forceinline__ void ladder_step_small(uint32_t (&X0)[L], uint32_t (&Z0)[L], uint32_t (&X1)[L],
+                                                  uint32_t (&Z1)[L], uint32_t c, const uint32_t (&N)[L],
+                                                  uint32_t n0inv, const F& f) {
+  uint32_t t1[L], t2[L], t3[L], t4[L], U[L], V[L], s[L], d[L];
+  f.add(t1, X0, Z0);
+  f.sub(t2, X0, Z0);
+  f.add(t3, X1, Z1);
+  f.sub(t4, X1, Z1);
+  f.mul(U, t2, t3);
+  f.mul(V, t1, t4);
+  f.sqr(s, t1);
+  f.sqr(d, t2);
+  f.mul(X0, s, d);
+  f.sub(t1, s, d);                  // t
+  mont_smul<L>(t2, c, t1, N, n0inv);  // a24 t
+  f.add(t2, d, t2);                 // d + a24 t
+  f.mul(Z0, t1, t2);
+  f.add(t3, U, V);
+  f.sub(t4, U, V);
+  f.sqr(X1, t3);
+  f.sqr(t4, t4);
+  f.add(Z1, t4, t4);                // x0 (U-V)^2 with x0 = 2
+}
+
 // The same step with a projective difference D = (Xd:Zd) (the paper-comparable prime-by-prime
 // schedule, reading G9b): X1' = Zd (U+V)^2, Z1' = Xd (U-V)^2 — 7M + 4S.
 template <int L, class F>
@@ -409,12 +436,34 @@ __device__ __forceinline__ uint8_t ecm_setup(const EcmParams& p, uint64_t sigma,
   return st;
 }
 
-// setup, and g = gcd(D, N) of a curve whose setup failed written at once (ecm_tail skips it)
+// Small-parameter family (reading G16 — not the paper's curves): a
+// seed s in [1, 2^30) gives a24 = s / 2^32 mod N and x0 = 2, both in Montgomery form; no
+// inversion.  Seeds outside the range get status 3 (g = N).
 template <int L>
+__device__ __forceinline__ uint8_t ecm_setup_small(const EcmParams& p, uint64_t seed, uint32_t (&x0)[L],
+                                                   uint32_t (&a24)[L]) {
+  const uint32_t(&N)[L] = cref<L>(p.N);
+  const uint32_t(&N2)[L] = cref<L>(p.N2);
+  const uint32_t(&ONE)[L] = cref<L>(p.ONE);
+  const bool ok = seed >= 1 && seed < (1ull << 30);
+  add_lazy<L>(x0, ONE, ONE, N2);                                 // 2 R mod N
+  mont_smul<L>(a24, ok ? (uint32_t)seed : 1u, ONE, N, p.n0inv);  // (s / 2^32) R mod N
+  return ok ? 0 : 3;
+}
+
+// setup, and g = gcd(D, N) of a curve whose setup failed written at once (ecm_tail skips it);
+// FAM 0: Brent-Suyama (the paper's), FAM 1: the small-parameter family
+template <int L, int FAM = 0>
 __device__ __forceinline__ uint8_t ecm_setup_store(const EcmParams& p, uint64_t sigma, uint32_t (&x0)[L],
                                                    uint32_t (&a24)[L], bool live, size_t i, uint32_t* g) {
   uint32_t gg[L];
-  const uint8_t st = ecm_setup<L>(p, sigma, x0, a24, gg);
+  uint8_t st;
+  if (FAM == 1) {
+    st = ecm_setup_small<L>(p, sigma, x0, a24);
+    copy(gg, cref<L>(p.N));
+  } else {
+    st = ecm_setup<L>(p, sigma, x0, a24, gg);
+  }
   if (live && st != 0) store<L>(g, i, gg);
   return st;
 }
@@ -466,7 +515,7 @@ __device__ __forceinline__ void ecm_tail(const EcmParams& p, const uint32_t (&X0
   status[i] = st;
 }
 
-template <int L, int VAR, bool EAGER, bool PRIMES>
+template <int L, int VAR, bool EAGER, bool PRIMES, int FAM>
 __global__ void __launch_bounds__(kEcmTPB, ecm_min_blocks(L, VAR, EAGER, PRIMES)) ecm_stage1_kernel(const __grid_constant__ EcmParams p,
                                                              const uint32_t* __restrict__ kwords, uint32_t k_bits,
                                                              const uint64_t* __restrict__ sigmas, size_t count,
@@ -484,7 +533,8 @@ __global__ void __launch_bounds__(kEcmTPB, ecm_min_blocks(L, VAR, EAGER, PRIMES)
   const uint64_t sigma = live ? sigmas[i] : 6ull;
 
   uint32_t X0[L], Z0[L], X1[L], Z1[L], x0[L], a24[L];
-  const uint8_t st = ecm_setup_store<L>(p, sigma, x0, a24, live, i, g);
+  const uint8_t st = ecm_setup_store<L, FAM>(p, sigma, x0, a24, live, i, g);
+  const uint32_t cs = st == 0 ? (uint32_t)sigma : 1u;  // FAM 1: a24 = cs / 2^32
 
   // ---------------- ladder over k (warp-uniform bits) ----------------
   if (EAGER) {
@@ -526,7 +576,8 @@ __global__ void __launch_bounds__(kEcmTPB, ecm_min_blocks(L, VAR, EAGER, PRIMES)
 #if ECM_CONST_SMEM
         ladder_step_sm<L, kEcmTPB>(X0, Z0, X1, Z1, &sm_c[0][0][threadIdx.x], &sm_c[1][0][threadIdx.x], fld);
 #else
-        ladder_step<L>(X0, Z0, X1, Z1, x0, a24, fld);
+        if (FAM == 1) ladder_step_small<L>(X0, Z0, X1, Z1, cs, N, n0inv, fld);
+        else ladder_step<L>(X0, Z0, X1, Z1, x0, a24, fld);
 #endif
 #endif
       }
@@ -640,7 +691,7 @@ __device__ __forceinline__ void ladder_step_coop(uint32_t (&X0)[L], uint32_t (&Z
   from_lane<L>(Z1, r, 1);
 }
 
-template <int L>
+template <int L, int FAM>
 __global__ void __launch_bounds__(kCoopTPB) ecm_stage1_coop_kernel(const __grid_constant__ EcmParams p,
                                                                    const uint32_t* __restrict__ kwords, uint32_t k_bits,
                                                                    const uint64_t* __restrict__ sigmas, size_t count,
@@ -659,7 +710,7 @@ __global__ void __launch_bounds__(kCoopTPB) ecm_stage1_coop_kernel(const __grid_
   const uint64_t sigma = live ? sigmas[i] : 6ull;
 
   uint32_t X0[L], Z0[L], X1[L], Z1[L], x0[L], a24[L];
-  const uint8_t st = ecm_setup_store<L>(p, sigma, x0, a24, live, i, g);
+  const uint8_t st = ecm_setup_store<L, FAM>(p, sigma, x0, a24, live, i, g);
   copy(X0, x0);
   copy(Z0, ONE);
   xdbl<L>(X1, Z1, X0, Z0, a24, fld);  // R1 = xDBL(P), replicated
@@ -692,7 +743,7 @@ __global__ void __launch_bounds__(kCoopTPB) ecm_stage1_coop_kernel(const __grid_
 // latency-bound up to one warp per sub-partition (profiles/r01_ecm_lat.jsonl).
 constexpr size_t kCoopMaxCurvesPerSM = 64;
 
-template <int L, int VAR, bool EAGER, bool PRIMES = false>
+template <int L, int VAR, bool EAGER, bool PRIMES = false, int FAM = 0>
 static cudaError_t launch_ecm_LV(const EcmParams& p, const uint32_t* kw, uint32_t k_bits, const uint64_t* sigmas,
                                  size_t count, uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status, uint32_t* xaff,
                                  uint32_t flags, cudaStream_t s) {
@@ -708,14 +759,14 @@ static cudaError_t launch_ecm_LV(const EcmParams& p, const uint32_t* kw, uint32_
     if (coop) {
       const size_t threads = count * kCoopLanes;
       const size_t blocks = (threads + kCoopTPB - 1) / kCoopTPB;
-      ecm_stage1_coop_kernel<L><<<(unsigned)blocks, kCoopTPB, 0, s>>>(p, kw, k_bits, sigmas, count, X, Z, g, status,
-                                                                      xaff, flags);
+      ecm_stage1_coop_kernel<L, FAM><<<(unsigned)blocks, kCoopTPB, 0, s>>>(p, kw, k_bits, sigmas, count, X, Z, g,
+                                                                           status, xaff, flags);
       return cudaGetLastError();
     }
   }
   const size_t blocks = (count + kEcmTPB - 1) / kEcmTPB;
-  ecm_stage1_kernel<L, VAR, EAGER, PRIMES><<<(unsigned)blocks, kEcmTPB, 0, s>>>(p, kw, k_bits, sigmas, count, X, Z, g,
-                                                                        status, xaff, flags);
+  ecm_stage1_kernel<L, VAR, EAGER, PRIMES, FAM><<<(unsigned)blocks, kEcmTPB, 0, s>>>(p, kw, k_bits, sigmas, count, X,
+                                                                             Z, g, status, xaff, flags);
   return cudaGetLastError();
 }
 
@@ -727,6 +778,11 @@ cudaError_t launch_ecm_L(const EcmParams& p, const uint32_t* kw, uint32_t k_bits
                                 uint32_t flags, cudaStream_t s) {
   const uint32_t var = (flags >> 8) & 7u;
   const bool eager = flags & 0x40u;
+  if (flags & 0x8000u) {  // small-parameter family: default lazy full-k ladder only
+    if (var == REDC_WORD && !eager && !(flags & 0x80u))
+      return launch_ecm_LV<L, REDC_WORD, false, false, 1>(p, kw, k_bits, sigmas, count, X, Z, g, status, xaff, flags, s);
+    return cudaErrorInvalidValue;
+  }
   if (flags & 0x80u) {  // prime-by-prime schedule (paper-comparable)
     if constexpr (L == 8) {
 #define ECM_PCASE(V, E) \

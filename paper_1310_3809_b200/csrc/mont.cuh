@@ -595,4 +595,27 @@ __device__ __forceinline__ void mont_mul(uint32_t (&r)[L], const uint32_t (&x)[L
   mont_mul_cios<L, REDC_WORD>(r, x, y, n, n0inv);
 }
 
+// r = c t / 2^32 mod N by one word-level REDC step, c < 2^30 a plain word, t < 2N: the product
+// of t (Montgomery form) with the field element c / 2^32 (the small-parameter family's a24,
+// SURVEY §8(f) N4) — 2L partial products instead of 2L^2.  c t + m N < 2^32 (1.5 N) < 2^32 R,
+// so the odd chains cannot carry out, and r < 1.5 N < 2N (lazy domain).
+template <int L>
+__device__ __forceinline__ void mont_smul(uint32_t (&r)[L], uint32_t c, const uint32_t (&t)[L],
+                                          const uint32_t (&n)[L], uint32_t n0inv) {
+  uint32_t E[L], O[L], Z[L];
+#pragma unroll
+  for (int k = 0; k < L; ++k) Z[k] = 0;
+  chain<L, 1, false, false>(O, Z, c, t);  // disjoint pairs on zero: no carries
+  chain<L, 0, false, false>(E, Z, c, t);
+  const uint32_t m = E[0] * n0inv;
+  chain<L, 1, false, false>(O, O, m, n);
+  chain<L, 0, false, true>(E, E, m, n);
+  O[L - 1] = ptx::addc(O[L - 1], 0u);
+  // (E + O 2^32) / 2^32 with E[0] == 0
+  r[0] = ptx::add_cc(O[0], E[1]);
+#pragma unroll
+  for (int k = 1; k < L - 1; ++k) r[k] = ptx::addc_cc(O[k], E[k + 1]);
+  r[L - 1] = ptx::addc(O[L - 1], 0u);
+}
+
 }  // namespace ecm

@@ -91,6 +91,11 @@ def test_argument_errors_before_any_device_work(L):
     assert lib.ecm_stage1_batch(Np, 6, 100, sp, 4, None, None, None, stp, None, 0x2000 | (3 << 8), None) == 1
     assert lib.ecm_mulmod_batch(p, p, p, p, 4, 6, 1, 0x2000, None) == 1
     assert lib.ecm_mulmod_batch(p, p, p, p, 4, 6, 1, 0x4000, None) == 1
+    # small-parameter family: default ladder only; not a mulmod flag
+    assert lib.ecm_stage1_batch(Np, 6, 100, sp, 4, None, None, None, stp, None, 0x8000 | 0x40, None) == 1
+    assert lib.ecm_stage1_batch(Np, 6, 100, sp, 4, None, None, None, stp, None, 0x8000 | 0x80, None) == 1
+    assert lib.ecm_stage1_batch(Np, 6, 100, sp, 4, None, None, None, stp, None, 0x8000 | (1 << 8), None) == 1
+    assert lib.ecm_mulmod_batch(p, p, p, p, 4, 6, 1, 0x8000, None) == 1
     kw = np.array([5], np.uint32)
     kp = kw.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
     assert lib.ecm_ladder_batch(Np, 6, kp, 4, sp, 4, None, None, None, stp, None, 0, None) == 4  # k_bits wrong

@@ -190,3 +190,51 @@ def test_c5_sampled_curves_full_b1(orc, torch):
     k, _ = orc.stage1_k(cfg["B1"])
     want = orc.ecm_stage1_mt(cfg["N"], 8, k, sig)
     assert_same(got, want)
+
+
+# --------------------------------------------------------------------------------------
+# small-parameter family (reading G16): a24 = s / 2^32, x0 = 2
+# --------------------------------------------------------------------------------------
+def small_seeds(sig):
+    """Seeds in [1, 2^30) derived from the configs' Suyama sigmas."""
+    return (np.asarray(sig, dtype=np.uint64) % np.uint64((1 << 30) - 1)) + np.uint64(1)
+
+
+@pytest.mark.parametrize("kernel", list(KERNELS))
+def test_small_family_c1_bit_exact(orc, torch, kernel):
+    cfg = ecm_config("C1")
+    k, _ = orc.stage1_k(cfg["B1"])
+    seeds = np.concatenate([small_seeds(cfg["sigmas"]), np.array([0, 1 << 30, 1, (1 << 30) - 1], np.uint64)])
+    got = gpu_stage1(torch, cfg["N"], 6, cfg["B1"], seeds, flags=eg.ECM_CURVE_SMALL | KERNELS[kernel])
+    want = orc.ecm_stage1_mt(cfg["N"], 6, k, seeds, family="small")
+    assert_same(got, want)
+    assert list(got["status"][-4:-2]) == [3, 3]
+    assert (got["status"] == 1).sum() >= 5
+
+
+@pytest.mark.parametrize("kernel", ["lanes1", "lanes4"])
+@pytest.mark.parametrize("L,nbits,pbits", [(4, 126, 30), (8, 254, 40), (12, 382, 40), (16, 510, 40)])
+def test_small_family_widths(orc, torch, L, nbits, pbits, kernel):
+    cfg = ecm_config(L=L, nbits=nbits, pbits=pbits, B1=400, curves=77, seed=50 + L)
+    k, _ = orc.stage1_k(cfg["B1"])
+    seeds = small_seeds(cfg["sigmas"])
+    got = gpu_stage1(torch, cfg["N"], L, cfg["B1"], seeds, flags=eg.ECM_CURVE_SMALL | KERNELS[kernel])
+    want = orc.ecm_stage1_mt(cfg["N"], L, k, seeds, family="small")
+    assert_same(got, want)
+
+
+def test_small_family_c3_sampled(orc, torch):
+    """C3's modulus and B1 with 2^18 small-family curves (the one-lane kernel at scale): 128
+    strided curves bit-exact, every flagged g divides N."""
+    cfg = ecm_config("C3")
+    seeds = small_seeds(cfg["sigmas"][: 1 << 18])
+    got = gpu_stage1(torch, cfg["N"], 6, cfg["B1"], seeds, flags=eg.ECM_CURVE_SMALL)
+    idx = np.linspace(0, seeds.size - 1, 128).astype(np.int64)
+    k, _ = orc.stage1_k(cfg["B1"])
+    want = orc.ecm_stage1_mt(cfg["N"], 6, k, seeds[idx], family="small")
+    assert_same({kk: v[idx] for kk, v in got.items()}, want)
+    flagged = np.nonzero(got["status"] == 1)[0]
+    assert flagged.size > 0
+    for i in flagged:
+        gi = eg.limbs_to_int(got["g"][i])
+        assert 1 < gi < cfg["N"] and cfg["N"] % gi == 0

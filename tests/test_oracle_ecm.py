@@ -257,3 +257,61 @@ def test_prime_schedule_small_field(orc, p):
             assert r["status"][0] == 2
         else:
             assert r["status"][0] == 0 and orc.from_limbs(r["xaff"][0]) == Q[0]
+
+
+# --------------------------------------------------------------------------------------
+# small-parameter family (reading G16): a24 = s / 2^32 mod N, x0 = 2
+# --------------------------------------------------------------------------------------
+def small_curve(p, s):
+    """(A, B) with P = (2, 1) on B y^2 = x^3 + A x^2 + x, A = 4 a24 - 2, a24 = s / 2^32 mod p."""
+    a24 = s * pow(1 << 32, -1, p) % p
+    A = (4 * a24 - 2) % p
+    B = (8 + 4 * A + 2) % p
+    if B == 0 or (A * A - 4) % p == 0:
+        return None
+    return A, B
+
+
+@pytest.mark.parametrize("p", SMALL_PRIMES[5::30])
+def test_small_family_matches_affine_group_law(orc, p):
+    """x([m]P) of the small-parameter family's ladder == the affine group law on the curve through
+    P = (2, 1), m = 1..40 and m = #E (Z = 0 exactly when ord(P) | m)."""
+    seen = 0
+    for s in (1, 2, 3, 17, 1000, (1 << 29) + 3, (1 << 30) - 1):
+        c = small_curve(p, s)
+        if c is None:
+            continue
+        A, B = c
+        P = (2, 1)
+        nE = count_points(A, B, p)
+        for m in list(range(1, 41)) + [nE]:
+            r = orc.ecm_stage1(p, 1, m, [s], family="small")
+            X, Z = orc.from_limbs(r["X"][0]), orc.from_limbs(r["Z"][0])
+            Q = aff_mul(m, P, A, B, p)
+            if Q is O:
+                assert Z == 0 and r["status"][0] == 2 and orc.from_limbs(r["g"][0]) == p
+            else:
+                assert Z != 0 and r["status"][0] == 0
+                assert X * pow(Z, -1, p) % p == Q[0] == orc.from_limbs(r["xaff"][0])
+        seen += 1
+    assert seen >= 4
+
+
+def test_small_family_seed_range_and_planted_factor(orc):
+    """Seeds outside [1, 2^30) are rejected per curve (status 3, g = N); on C1's modulus the
+    family finds the planted 32-bit prime on some curves, and every g divides N."""
+    cfg = ecm_config("C1")
+    N, p = cfg["N"], cfg["p"]
+    k, _ = orc.stage1_k(cfg["B1"])
+    r = orc.ecm_stage1(N, 6, k, [0, 1 << 30, (1 << 62) + 5], family="small")
+    assert list(r["status"]) == [3, 3, 3]
+    assert all(orc.from_limbs(g) == N for g in r["g"])
+    seeds = np.arange(1, 257, dtype=np.uint64) * 4099
+    r = orc.ecm_stage1_mt(N, 6, k, seeds, family="small")
+    found = r["status"] == 1
+    assert found.sum() >= 5
+    for g, st in zip(r["g"], r["status"]):
+        gi = orc.from_limbs(g)
+        assert N % gi == 0
+        if st == 1:
+            assert gi == p
