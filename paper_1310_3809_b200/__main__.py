@@ -1,7 +1,8 @@
 """Command-line interface (mirroring SPEC S:500-566 for this path).
 
     python -m paper_1310_3809_b200 factor --n HEX [--b1 B1] [--curves C] [--seed S] [--L L]
-                                          [--schedule full|primes] [--format text|jsonl]
+                                          [--schedule full|primes] [--family suyama|small]
+                                          [--format text|jsonl]
     python -m paper_1310_3809_b200 mulmod --L L --count C --iters K [--seed S] [--square]
     python -m paper_1310_3809_b200 version
 
@@ -20,7 +21,7 @@ EXIT_OK, EXIT_INPUT, EXIT_NOFACTOR = 0, 1, 2
 
 
 def _pick_L(n: int) -> int | None:
-    for L in (4, 6, 8, 12):
+    for L in (4, 6, 8, 12, 16):
         if n.bit_length() <= 32 * L - 2:
             return L
     return None
@@ -43,13 +44,19 @@ def cmd_factor(a) -> int:
         return EXIT_INPUT
     L = a.L or _pick_L(n)
     if L is None or n.bit_length() > 32 * L - 2:
-        print("error: n is wider than 382 bits (L = 12, two spare bits)", file=sys.stderr)
+        print("error: n is wider than 510 bits (L = 16, two spare bits)", file=sys.stderr)
         return EXIT_INPUT
     if a.b1 < 2 or a.curves < 1:
         print("error: need B1 >= 2 and curves >= 1", file=sys.stderr)
         return EXIT_INPUT
     sig = make_sigmas(a.seed, a.curves)
     flags = eg.ECM_PRIME_LADDERS if a.schedule == "primes" else 0
+    if a.family == "small":  # §8(f) N4 curves: seeds in [1, 2^30)
+        if a.schedule == "primes":
+            print("error: --family small needs --schedule full", file=sys.stderr)
+            return EXIT_INPUT
+        sig = (sig % np.uint64((1 << 30) - 1)) + np.uint64(1)
+        flags |= eg.ECM_CURVE_SMALL
     if torch.cuda.is_available():
         r = eg.ecm_stage1_batch(n, L, a.b1, torch.from_numpy(sig).cuda(), flags=flags, want=("g",))
         status = r["status"].cpu().numpy()
@@ -108,6 +115,8 @@ def main(argv=None) -> int:
     f.add_argument("--seed", type=int, default=1)
     f.add_argument("--L", type=int, default=None)
     f.add_argument("--schedule", choices=["full", "primes"], default="full")
+    f.add_argument("--family", choices=["suyama", "small"], default="suyama",
+                   help="curve family: the paper's Brent-Suyama curves, or the small-parameter family")
     f.add_argument("--format", choices=["text", "jsonl"], default="text")
     m = sub.add_parser("mulmod", help="time one batched Montgomery chain")
     m.add_argument("--L", type=int, default=6)

@@ -17,7 +17,8 @@ def _cli(*args, timeout=600):
 def test_cli_input_errors():
     assert _cli("factor", "--n", "xyz").returncode == 1
     assert _cli("factor", "--n", "10").returncode == 1          # even
-    assert _cli("factor", "--n", "f" * 100).returncode == 1     # 400 bits > 382
+    assert _cli("factor", "--n", "f" * 130).returncode == 1     # 520 bits > 510
+    assert _cli("factor", "--n", "8f", "--family", "small", "--schedule", "primes").returncode == 1
     assert _cli("factor", "--n", "8f", "--b1", "1").returncode == 1
 
 
@@ -42,6 +43,8 @@ def test_cli_and_c_example_find_planted_factor():
     assert r.returncode == 0, r.stderr
     assert str(cfg["p"]) in r.stdout
     r = _cli("factor", "--n", f"{cfg['N']:x}", "--b1", "2000", "--curves", "256", "--schedule", "primes")
+    assert r.returncode == 0 and str(cfg["p"]) in r.stdout
+    r = _cli("factor", "--n", f"{cfg['N']:x}", "--b1", "2000", "--curves", "256", "--family", "small")
     assert r.returncode == 0 and str(cfg["p"]) in r.stdout
     exe = _build_c_example()
     out = subprocess.run([exe, f"{cfg['N']:x}", "2000", "256", "7"], capture_output=True, text=True, timeout=300)
