@@ -50,14 +50,15 @@ int main(int argc, char **argv) {
     fprintf(stderr, "usage: %s <hex N> [B1] [curves] [seed]\n", argv[0]);
     return 1;
   }
-  uint32_t N[12];
-  const int bl = parse_hex(argv[1], N, 12);
+  uint32_t N[16];
+  const int bl = parse_hex(argv[1], N, 16);
   const uint64_t B1 = argc > 2 ? strtoull(argv[2], 0, 10) : 2000;
   const size_t curves = argc > 3 ? strtoull(argv[3], 0, 10) : 256;
   uint64_t seed = argc > 4 ? strtoull(argv[4], 0, 10) : 1;
   int L = 0;
-  for (int c = 4; c <= 12 && !L; c += (c < 8 ? 2 : 4))
-    if (bl > 0 && bl <= 32 * c - 2) L = c;
+  static const int widths[] = {4, 6, 8, 12, 16};
+  for (int j = 0; j < 5 && !L; ++j)
+    if (bl > 0 && bl <= 32 * widths[j] - 2) L = widths[j];
   if (!L || curves == 0) {
     fprintf(stderr, "bad input\n");
     return 1;
