@@ -41,7 +41,7 @@ extern "C" {
 
 typedef enum {
   ECM_OK = 0,
-  ECM_E_ARG = 1,     /* null pointer, count == 0, unsupported L, misaligned pointer, bad flags */
+  ECM_E_ARG = 1,     /* null pointer, count == 0 or > 2^40, unsupported L, misaligned pointer, bad flags */
   ECM_E_MODULUS = 2, /* N even or N < 3 (ECM_CHECK for mulmod; always for stage 1) */
   ECM_E_WIDTH = 3,   /* bitlen(N) > 32L-2: no two spare bits */
   ECM_E_B1 = 4,      /* B1 < 2 or B1 >= 2^32, or k_bits == 0 */

@@ -34,6 +34,9 @@ constexpr uint32_t kKnownFlags = ECM_CANONICAL | ECM_SQUARE | ECM_LAYOUT_SLICED 
 // L = 16 ladder kernel holds its six-residue state in 254 registers without spilling)
 bool valid_L(int L) { return L == 4 || L == 6 || L == 8 || L == 12 || L == 16; }
 bool valid_L_mulmod(int L) { return valid_L(L); }
+// count small enough that every byte size the calls form (4 arrays x count x L words, and the
+// kernels' element indices) fits size_t with room: 2^40 elements (far beyond device memory)
+bool valid_count(size_t count) { return count != 0 && count <= ((size_t)1 << 40); }
 
 // ---- host multiprecision helpers (little-endian 32-bit words, fixed width W) ----
 int bitlen(const uint32_t* a, int W) {
@@ -333,7 +336,7 @@ uint32_t ecm_stage1_kbits(uint64_t B1) {
 ecm_status ecm_mulmod_batch(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out, size_t count,
                             int L, uint32_t iters, uint32_t flags, void* stream) {
   const bool square = flags & ECM_SQUARE;
-  if (!a || !n || !out || (!b && !square) || count == 0 || !valid_L_mulmod(L) || iters == 0 ||
+  if (!a || !n || !out || (!b && !square) || !valid_count(count) || !valid_L_mulmod(L) || iters == 0 ||
       (flags & ~kKnownFlags))
     return ECM_E_ARG;
   if (flags & (ECM_NO_XAFF | ECM_EAGER | ECM_PRIME_LADDERS | ECM_KERNEL_LANES4 | ECM_KERNEL_LANES1 | ECM_CURVE_SMALL))
@@ -394,7 +397,7 @@ ecm_status ecm_mulmod_batch(const uint32_t* a, const uint32_t* b, const uint32_t
 ecm_status ecm_stage1_batch(const uint32_t* N_host, int L, uint64_t B1, const uint64_t* sigmas, size_t count,
                             uint32_t* X, uint32_t* Z, uint32_t* g, uint8_t* status, uint32_t* xaff, uint32_t flags,
                             void* stream) {
-  if (!N_host || !sigmas || !status || count == 0 || !valid_L(L) || (flags & ~kKnownFlags)) return ECM_E_ARG;
+  if (!N_host || !sigmas || !status || !valid_count(count) || !valid_L(L) || (flags & ~kKnownFlags)) return ECM_E_ARG;
   if (flags & (ECM_SQUARE | ECM_LAYOUT_SLICED | ECM_CANONICAL | ECM_KERNEL_STREAM | ECM_KERNEL_WARP)) return ECM_E_ARG;
   if (!ecm_variant_ok(L, flags)) return ECM_E_ARG;
   if (!xaff && !(flags & ECM_NO_XAFF)) flags |= ECM_NO_XAFF;
@@ -429,7 +432,7 @@ ecm_status ecm_stage1_batch(const uint32_t* N_host, int L, uint64_t B1, const ui
 ecm_status ecm_ladder_batch(const uint32_t* N_host, int L, const uint32_t* k_words, uint32_t k_bits,
                             const uint64_t* sigmas, size_t count, uint32_t* X, uint32_t* Z, uint32_t* g,
                             uint8_t* status, uint32_t* xaff, uint32_t flags, void* stream) {
-  if (!N_host || !k_words || !sigmas || !status || count == 0 || !valid_L(L) || (flags & ~kKnownFlags))
+  if (!N_host || !k_words || !sigmas || !status || !valid_count(count) || !valid_L(L) || (flags & ~kKnownFlags))
     return ECM_E_ARG;
   if (flags & (ECM_SQUARE | ECM_LAYOUT_SLICED | ECM_CANONICAL | ECM_KERNEL_STREAM | ECM_KERNEL_WARP)) return ECM_E_ARG;
   if (!ecm_variant_ok(L, flags)) return ECM_E_ARG;

@@ -58,6 +58,7 @@ def test_argument_errors_before_any_device_work(L):
     # unsupported L, count 0, null pointers, unknown flags, iters 0
     assert lib.ecm_mulmod_batch(p, p, p, p, 4, 5, 1, 0, None) == 1
     assert lib.ecm_mulmod_batch(p, p, p, p, 0, 6, 1, 0, None) == 1
+    assert lib.ecm_mulmod_batch(p, p, p, p, (1 << 62) + 1, 6, 1, 0, None) == 1  # size overflow guard
     assert lib.ecm_mulmod_batch(None, p, p, p, 4, 6, 1, 0, None) == 1
     assert lib.ecm_mulmod_batch(p, None, p, p, 4, 6, 1, 0, None) == 1
     assert lib.ecm_mulmod_batch(p, p, p, p, 4, 6, 1, 1 << 20, None) == 1
