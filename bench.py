@@ -155,6 +155,16 @@ def ncu_traffic(name):
 CPU_TARGET_S = 10.0  # bounded oracle sample: about 10 s of host work per baseline
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def cpu_baseline_mulmod(sample_elems: int, iters: int, target_s: float = CPU_TARGET_S):
     """The oracle as it stands on all host cores, over consecutive C2 triples: at least
     `sample_elems`, then further chunks until about `target_s` seconds have elapsed."""
@@ -171,7 +181,7 @@ def cpu_baseline_mulmod(sample_elems: int, iters: int, target_s: float = CPU_TAR
         done += chunk
     return {"value": done * iters / dt, "unit": "modmul/s", "cores": threads, "kind": "oracle",
             "sample": f"first {done} of C2's 2^24 triples x K={iters} (oracle C, {threads} host threads)",
-            "seconds": dt}
+            "seconds": dt, "per_core": done * iters / dt / threads, "cpu": cpu_model()}
 
 
 def cpu_baseline_ecm(N, k, sigmas, B1, target_s: float = CPU_TARGET_S):
@@ -187,7 +197,8 @@ def cpu_baseline_ecm(N, k, sigmas, B1, target_s: float = CPU_TARGET_S):
         dt += time.perf_counter() - t0
         done += len(part)
     return {"value": done / dt, "unit": "curves/s", "cores": threads, "kind": "oracle",
-            "sample": f"{done} strided curves of C3 at B1={B1}", "seconds": dt}
+            "sample": f"{done} strided curves of C3 at B1={B1}", "seconds": dt, "per_core": done / dt / threads,
+            "cpu": cpu_model()}
 
 
 # ---------------------------------------------------------------------------------------
