@@ -9,8 +9,11 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = pytest.mark.gpu
-SMALL = ["--steps", "2", "--warmup", "3", "--count", "65536", "--iters", "8", "--ecm-curves", "2048",
-         "--ecm-b1", "300", "--no-sweep"]
+BASE = ["--steps", "2", "--warmup", "3", "--count", "65536", "--iters", "8", "--ecm-curves", "2048",
+        "--ecm-b1", "300"]
+SMALL = BASE + ["--no-sweep"]
+# the sweeps too (mulmod widths, K = 1, ECM widths, the small-parameter family), shortened
+SWEEP = BASE + ["--ecm-width-curves", "1024"]
 
 
 def _one_line(out):
@@ -30,13 +33,17 @@ def test_bench_single_rank_small():
         assert k in d
 
 
-def test_bench_two_ranks_torchrun_gloo():
+@pytest.mark.parametrize("args", [SMALL, SWEEP], ids=["no-sweep", "sweep"])
+def test_bench_two_ranks_torchrun_gloo(args):
     env = dict(os.environ, ECM_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "bench.py"), "--gpus", "2",
-           *SMALL]
+           *args]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     d = _one_line(r.stdout)
     assert d["n_gpus"] == 2 and d["value"] > 0 and "cpu_baseline" not in d
     assert d["ecm"]["flagged_factor"] >= 0
+    if args is SWEEP:
+        assert set(d["ecm"]["widths"]) == {"L4", "L6", "L8", "L12", "L16"}
+        assert d["ecm"]["small_family"]["curves_per_s"] > 0 and "mul_L16" in d["sweep"]

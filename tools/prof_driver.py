@@ -6,6 +6,7 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import paper_1310_3809_b200 as eg  # noqa: E402
@@ -31,8 +32,11 @@ if a.what == "mulmod":
         eg.ecm_mulmod_batch(x, y, n, L=a.L, iters=a.iters, flags=fl)
 else:
     cfg = ecm_config(a.cfg)
-    s = torch.from_numpy(cfg["sigmas"][: a.curves].copy()).cuda()
+    sig = cfg["sigmas"][: a.curves].copy()
+    if a.flags & eg.ECM_CURVE_SMALL:
+        sig = (sig % np.uint64((1 << 30) - 1)) + np.uint64(1)
+    s = torch.from_numpy(sig).cuda()
     for _ in range(a.reps):
-        eg.ecm_stage1_batch(cfg["N"], 6, a.B1, s, want=("g",))
+        eg.ecm_stage1_batch(cfg["N"], 6, a.B1, s, flags=a.flags, want=("g",))
 torch.cuda.synchronize()
 print("done")

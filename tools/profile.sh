@@ -26,5 +26,7 @@ cap k1 mulmod_ mulmod --iters 1 --reps 1
 cap k1_sliced mulmod_ mulmod --sliced --iters 1 --reps 1
 cap ecm ecm_stage1_kernel ecm --curves 1048576 --B1 2000 --reps 1
 cap ecm_c1 ecm_stage1_coop ecm --cfg C1 --curves 256 --B1 2000 --reps 1
+cap ecm_small ecm_stage1_kernel ecm --curves 1048576 --B1 2000 --flags 32768 --reps 1
+cap mulmod_l16 mulmod_batch_kernel mulmod --sliced --L 16 --count 4194304 --reps 1
 fi
 ls -la $OUT
