@@ -38,6 +38,11 @@ constexpr int kEcmTPB = 128;
 #ifndef ECM_CONST_SMEM
 #define ECM_CONST_SMEM 0
 #endif
+//   ECM_LADDER_UNROLL : unroll factor of the one-lane ladder loop
+#ifndef ECM_LADDER_UNROLL
+#define ECM_LADDER_UNROLL 1
+#endif
+constexpr int kLadderUnroll = ECM_LADDER_UNROLL;
 // Occupancy of the default ladder (tools/ecm_ab.py, profiles/r01_ecm_ab.jsonl): L <= 6 is held to
 // 80 registers = 6 CTAs x 4 warps per SM (at 81..88 the 256-register warp allocation granule leaves
 // 5; the cap costs one spill load per step); L = 12 to 168 = 3 CTAs (+6 % over 182 registers and 2
@@ -555,6 +560,7 @@ __global__ void __launch_bounds__(kEcmTPB, ecm_min_blocks(L, VAR, EAGER, PRIMES)
       int idx = (int)k_bits - 2;
       int chunk = idx >> 10;  // 32 words = 1024 bits per warp-wide load
       uint32_t kreg = kwords[(chunk << 5) + lane];
+#pragma unroll kLadderUnroll
       for (; idx >= 0; --idx) {
         if ((idx >> 10) != chunk) {
           chunk = idx >> 10;
