@@ -28,6 +28,8 @@ constexpr int kMulmodTPB = 256;
 // Chain-loop unroll and the limb-sliced L <= 6 kernels' occupancy (tools/ecm_ab.py variants,
 // DESIGN.md §6.2): unrolled by 8 and held to 64 registers (4 CTAs x 8 warps per SM), the L = 6
 // sliced chains measured +0.6 % (multiply) and +3.5 % (square) over unroll 4 / 76 registers.
+// Per width (multiply / square, word REDC): L = 4: 8 / 16, L = 6: 8 / 8, L = 8: 2 / 8,
+// L = 12, 16: 2 / 2 — each the best of {2, 4, 8, 16} measured; other REDC variants keep 4.
 // MULMOD_UNROLL / MULMOD_SLICED_MINB override them for experiments.
 #ifndef MULMOD_UNROLL
 #define MULMOD_UNROLL 0  // 0: per-width default below
@@ -35,8 +37,13 @@ constexpr int kMulmodTPB = 256;
 #ifndef MULMOD_SLICED_MINB
 #define MULMOD_SLICED_MINB 4
 #endif
-__host__ __device__ constexpr int mulmod_unroll(int L, int V) {
-  return MULMOD_UNROLL > 0 ? MULMOD_UNROLL : (L <= 6 && V == 0) ? 8 : 4;
+__host__ __device__ constexpr int mulmod_unroll(int L, int V, bool square) {
+  return MULMOD_UNROLL > 0 ? MULMOD_UNROLL
+         : V != 0        ? 4
+         : L <= 4        ? (square ? 16 : 8)
+         : L <= 6        ? 8
+         : L <= 8        ? (square ? 8 : 2)
+                         : 2;
 }
 __host__ __device__ constexpr int mulmod_min_blocks(int L, int V, bool sliced) {
   return (!sliced && V == 0 && L <= 6) ? 6 : (sliced && V == 0 && L <= 6) ? MULMOD_SLICED_MINB : 1;
@@ -176,7 +183,7 @@ __device__ __forceinline__ void mulmod_chain(uint32_t (&x)[L], const uint32_t (&
   uint32_t np[L], dN[L / 2], sn = 0;
   if (V == REDC_BLOCKTHM || V == REDC_CLASSIC || V == REDC_KARATSUBA) nprime_full<L>(np, nn);
   if (V == REDC_KARATSUBA) kara_consts<L>(dN, sn, nn);
-  constexpr int kUnroll = mulmod_unroll(L, V);
+  constexpr int kUnroll = mulmod_unroll(L, V, SQUARE);
 #pragma unroll kUnroll
   for (uint32_t t = iters; t != 0; --t) {
     uint32_t r[L];
