@@ -650,6 +650,13 @@ __device__ __forceinline__ void pick4(uint32_t (&d)[L], int q, const uint32_t (&
   }
 }
 
+// d = c ? a1 : a0 with an all-ones/zero mask c, 1 LOP3 per word
+template <int L>
+__device__ __forceinline__ void pick2(uint32_t (&d)[L], uint32_t c, const uint32_t (&a0)[L], const uint32_t (&a1)[L]) {
+#pragma unroll
+  for (int k = 0; k < L; ++k) d[k] = (a0[k] & ~c) | (a1[k] & c);
+}
+
 template <int L>
 __device__ __forceinline__ void from_lane(uint32_t (&d)[L], const uint32_t (&r)[L], int q) {
 #pragma unroll
@@ -667,7 +674,7 @@ __device__ __forceinline__ void ladder_step_coop(uint32_t (&X0)[L], uint32_t (&Z
   add_lazy<L>(t3, X1, Z1, N2);
   sub_lazy<L>(t4, X1, Z1, N2);
   // round A: U = t2 t3, V = t1 t4, s = t1^2, d = t2^2
-  pick4<L>(a, q, t2, t1, t1, t2);
+  pick2<L>(a, 0u - (uint32_t)((q ^ (q >> 1)) & 1), t2, t1);  // t1 for q = 1, 2
   pick4<L>(b, q, t3, t4, t1, t2);
   mont_mul<L>(r, a, b, N, n0inv);
   uint32_t U[L], V[L], sd[L], dd[L];
@@ -690,8 +697,9 @@ __device__ __forceinline__ void ladder_step_coop(uint32_t (&X0)[L], uint32_t (&Z
   from_lane<L>(sq, r, 3);
   add_lazy<L>(w1, dd, at, N2);  // d + a24 t
   // round C: Z0' = t (d + a24 t), Z1' = x0 (U-V)^2 (lanes 2, 3 repeat lanes 0, 1)
-  pick4<L>(a, q, tt, x0, tt, x0);
-  pick4<L>(b, q, w1, sq, w1, sq);
+  const uint32_t odd = 0u - (uint32_t)(q & 1);
+  pick2<L>(a, odd, tt, x0);
+  pick2<L>(b, odd, w1, sq);
   mont_mul<L>(r, a, b, N, n0inv);
   from_lane<L>(Z0, r, 0);
   from_lane<L>(Z1, r, 1);
