@@ -20,7 +20,7 @@
 // (O[k] has weight 2^(32(k+1))).  Within a row no two pairs overlap, so each accumulator is
 // ONE carry chain of L/2 IMAD.WIDE.  The division by 2^32 at the end of a CIOS row is pure
 // register renaming: the next row's odd chain reads E[2..L) as its addends (the "shift").
-// L must be even (L in {4, 6, 8, 12}).
+// L must be even (L in {4, 6, 8, 12, 16}).
 #pragma once
 #include <cstdint>
 
