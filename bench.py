@@ -202,6 +202,15 @@ def cpu_baseline_ecm(N, k, sigmas, B1, target_s: float = CPU_TARGET_S):
 
 
 # ---------------------------------------------------------------------------------------
+def c2_config(count, iters, ws):
+    """The C2 workload both arms report (the reference arm processes a bounded sample of it per step,
+    described in its cpu_baseline)."""
+    return {"workload": f"C2: {count} independent (a,b,N) triples per GPU, L=6 (190-bit N), "
+                        f"K={iters} chained lazy Montgomery products", "L": L, "count_per_gpu": count,
+            "iters": iters, "redc": "word-CIOS (default)", "layout": "limb-sliced [j*count+i]",
+            "l2": "inputs 1.15 GiB > L2 (no flush needed)", "parallelism": f"replicas x{ws}"}
+
+
 def run_ours(args):
     import torch
     ws, rank, local = dist_env()
@@ -422,11 +431,7 @@ def run_ours(args):
         "value": value, "unit": "modmul/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": f"C2: {count} independent (a,b,N) triples per GPU, L=6 (190-bit N), "
-                               f"K={args.iters} chained lazy Montgomery products", "L": L, "count_per_gpu": count,
-                   "iters": args.iters, "redc": "word-CIOS (default)", "layout": "limb-sliced [j*count+i]",
-                   "l2": "inputs 1.15 GiB > L2 (no flush needed)",
-                   "parallelism": f"replicas x{ws}"},
+        "config": c2_config(count, args.iters, ws),
         "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": pk["fpe_peak"] / 1e12, "unit": "Tpp/s",
                      "frac": achieved / pk["fpe_peak"], "traffic": ncu_traffic("mulmod_batch_kernel<6,0,false,true>"),
                      "kernel": "ecm::mulmod_batch_kernel<6,0,false,true>", "kernel_ms": kernel_ms,
@@ -493,8 +498,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": "192-bit Montgomery modmul/s", "value": value, "unit": "modmul/s",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"C2 sample: {sample} of the 2^24 triples per step, L=6, K={args.iters}",
-                       "L": L, "iters": args.iters},
+            "config": c2_config(args.count, args.iters, ws),
             "cpu_baseline": cb, "e2e": {"value": value, "unit": "modmul/s", "h2d_bytes_per_step": 0,
                                         "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
