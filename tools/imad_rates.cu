@@ -67,6 +67,10 @@ __global__ void bench_dfma(uint32_t* out, uint32_t seed, long long* cyc) {
 template <int MODE>
 __global__ void bench(uint32_t* out, uint32_t seed, long long* cyc) {
   uint32_t x[CHAINS], y[CHAINS], z[CHAINS];
+  double fx[CHAINS];
+#pragma unroll
+  for (int c = 0; c < CHAINS; ++c) fx[c] = 1.0 + 1e-9 * (threadIdx.x + c);
+  const double fa = 0.999999 + 1e-12 * seed, fb = 1e-7 * threadIdx.x;
 #pragma unroll
   for (int c = 0; c < CHAINS; ++c) { x[c] = seed + threadIdx.x * 7 + c; y[c] = x[c] ^ 0x5bd1e995u; z[c] = c; }
   uint32_t a = seed * 3 + 1 + threadIdx.x * 2, b = (seed ^ 0x9e3779b9u) + threadIdx.x;
@@ -84,13 +88,16 @@ __global__ void bench(uint32_t* out, uint32_t seed, long long* cyc) {
       if (MODE == 6) { if ((c & 3) == 0) { uint32_t bb[4] = {y[c], y[c+1], y[c+2], y[c+3]}; imad_row4(&x[c & 0], x[(c + 4) & 7] ^ a, bb); } lop3(z[c], a, b); }   // fma + alu co-issue
       if (MODE == 7) addcc(x[c], y[c], a, b);
       if (MODE == 8) { imad_lo(x[c], a, b); lop3(z[c], a, b); }
+      // FP64 next to IMAD.WIDE: does the fp64 pipe run concurrently with the fma-heavy products?
+      if (MODE == 9) { if ((c & 3) == 0) { uint32_t bb[4] = {y[c], y[c+1], y[c+2], y[c+3]}; imad_row4(&x[c & 0], x[(c + 4) & 7] ^ a, bb); } dfma(fx[c], fa, fb); }
+      if (MODE == 10) { if ((c & 3) == 0) { uint32_t bb[4] = {y[c], y[c+1], y[c+2], y[c+3]}; imad_row4(&x[c & 0], x[(c + 4) & 7] ^ a, bb); } if (c & 1) dfma(fx[c], fa, fb); }
     }
   }
   __syncthreads();
   long long t1 = clock64();
   uint32_t s = 0;
 #pragma unroll
-  for (int c = 0; c < CHAINS; ++c) s ^= x[c] ^ y[c] ^ z[c];
+  for (int c = 0; c < CHAINS; ++c) s ^= x[c] ^ y[c] ^ z[c] ^ (uint32_t)(fx[c] * 7.0);
   if (s == 0x12345678u) out[0] = s;
   if (threadIdx.x == 0) atomicMax((unsigned long long*)cyc, (unsigned long long)(t1 - t0));
 }
@@ -133,6 +140,8 @@ int main() {
   run<6>("IMAD.WIDE rows + LOP3", 1, nsm, 256, 4);
   run<7>("IADD3+IADD3.X pairs", 2, nsm, 256, 4);
   run<8>("IMAD+LOP3", 1, nsm, 256, 4);
+  run<9>("IMAD.WIDE rows + DFMA (1:1)", 1, nsm, 256, 4);
+  run<10>("IMAD.WIDE rows + DFMA (2:1)", 1, nsm, 256, 4);
   {
     uint32_t* out; long long* cyc; cudaMalloc(&out, 4); cudaMalloc(&cyc, 8);
     const int grid = nsm * 4, threads = 256;
