@@ -14,7 +14,7 @@ import paper_1310_3809_b200 as eg  # noqa: E402
 from workload import ecm_config, mulmod_inputs  # noqa: E402
 
 torch.cuda.set_device(0)
-for L in (4, 6, 8, 12):
+for L in (4, 6, 8, 12, 16):
     a, b, n = mulmod_inputs(32 * 3 + 5, L, seed=L, lazy=True)
     A, B, N = (torch.from_numpy(x).cuda() for x in (a, b, n))
     for fl in (0, eg.ECM_SQUARE, eg.ECM_CANONICAL, eg.ECM_CHECK, eg.ECM_REDC_KNOWNLOW, eg.ECM_REDC_BLOCKTHM,
@@ -27,6 +27,9 @@ for L in (4, 6, 8, 12):
     s = torch.from_numpy(cfg["sigmas"]).cuda()
     eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], s)  # small batch: the 4-lane kernel
     eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], s, flags=eg.ECM_KERNEL_LANES1)
+    seeds = torch.from_numpy((cfg["sigmas"] % np.uint64((1 << 30) - 1)) + np.uint64(1)).cuda()
+    for fl in (0, eg.ECM_KERNEL_LANES1):  # the small-parameter family (§8(f) N4), both kernels
+        eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], seeds, flags=eg.ECM_CURVE_SMALL | fl)
     eg.ecm_ladder_batch(cfg["N"], L, 12345, s)
     if L in (6, 8):
         for fl in (eg.ECM_EAGER, eg.ECM_REDC_CLASSIC, eg.ECM_PRIME_LADDERS):
