@@ -191,12 +191,14 @@ struct Field {
   __device__ __forceinline__ void mul(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L]) const {
     if (V == REDC_WORD || V == REDC_KNOWNLOW) mont_mul_cios<L, V>(r, x, y, N, n0inv);
     else mont_mul_block<L, V>(r, x, y, N, NP);
+    debug_lazy_bound<L>(r, N);
     if (EAGER) canonicalize<L>(r, r, N);
   }
   __device__ __forceinline__ void sqr(uint32_t (&r)[L], const uint32_t (&x)[L]) const {
     if (V == REDC_WORD) mont_sqr<L>(r, x, N, n0inv);
     else if (V == REDC_KNOWNLOW) mont_mul_cios<L, V>(r, x, x, N, n0inv);
     else mont_mul_block<L, V>(r, x, x, N, NP);
+    debug_lazy_bound<L>(r, N);
     if (EAGER) canonicalize<L>(r, r, N);
   }
   __device__ __forceinline__ void add(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L]) const {

@@ -589,10 +589,36 @@ __device__ __forceinline__ void canonicalize(uint32_t (&r)[L], const uint32_t (&
   for (int k = 0; k < L; ++k) r[k] = borrow ? x[k] : d[k];
 }
 
+// Debug builds (-DECM_DEBUG_BOUNDS=1, tools/debug_bounds.py) check the Lemma's lazy bound r < 2N
+// (reading G3) after every Montgomery product and trap if it fails.
+#ifndef ECM_DEBUG_BOUNDS
+#define ECM_DEBUG_BOUNDS 0
+#endif
+template <int L>
+__device__ __forceinline__ void debug_lazy_bound(const uint32_t (&r)[L], const uint32_t (&n)[L]) {
+#if ECM_DEBUG_BOUNDS
+  uint32_t n2[L], c = 0;
+#pragma unroll
+  for (int k = 0; k < L; ++k) {
+    n2[k] = (n[k] << 1) | c;
+    c = n[k] >> 31;
+  }
+  int cmp = 0;  // sign of r - 2N, decided from the top word down
+#pragma unroll
+  for (int k = L - 1; k >= 0; --k)
+    if (cmp == 0 && r[k] != n2[k]) cmp = r[k] < n2[k] ? -1 : 1;
+  if (cmp >= 0) __trap();
+#else
+  (void)r;
+  (void)n;
+#endif
+}
+
 template <int L>
 __device__ __forceinline__ void mont_mul(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L],
                                          const uint32_t (&n)[L], uint32_t n0inv) {
   mont_mul_cios<L, REDC_WORD>(r, x, y, n, n0inv);
+  debug_lazy_bound<L>(r, n);
 }
 
 // r = c t / 2^32 mod N by one word-level REDC step, c < 2^30 a plain word, t < 2N: the product
@@ -616,6 +642,7 @@ __device__ __forceinline__ void mont_smul(uint32_t (&r)[L], uint32_t c, const ui
 #pragma unroll
   for (int k = 1; k < L - 1; ++k) r[k] = ptx::addc_cc(O[k], E[k + 1]);
   r[L - 1] = ptx::addc(O[L - 1], 0u);
+  debug_lazy_bound<L>(r, n);
 }
 
 }  // namespace ecm

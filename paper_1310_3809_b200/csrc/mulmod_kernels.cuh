@@ -198,6 +198,7 @@ __device__ __forceinline__ void mulmod_chain(uint32_t (&x)[L], const uint32_t (&
       if (SQUARE) mont_mul_block<L, V>(r, x, x, nn, np);
       else mont_mul_block<L, V>(r, x, y, nn, np);
     }
+    debug_lazy_bound<L>(r, nn);
 #pragma unroll
     for (int k = 0; k < L; ++k) x[k] = r[k];
   }

@@ -21,13 +21,14 @@ VAR = os.path.join(ROOT, "tools", "_variants")
 
 
 def build(pairs, L=6):
-    """Variant NAME = the product objects with ecm_l<L>.cu and mulmod_l<L>.cu recompiled with FLAGS."""
+    """Variant NAME = the product objects with ecm_l<L>.cu and mulmod_l<L>.cu (L = 0: every .cu)
+    recompiled with FLAGS."""
     import concurrent.futures as cf
     from paper_1310_3809_b200 import build as B
     B.build()
     os.makedirs(VAR, exist_ok=True)
     objs = sorted(os.path.join(B.BUILD, f) for f in os.listdir(B.BUILD) if f.endswith(".o"))
-    srcs = [f"ecm_l{L}.cu", f"mulmod_l{L}.cu"]
+    srcs = [f"ecm_l{L}.cu", f"mulmod_l{L}.cu"] if L else sorted(f for f in os.listdir(B.CSRC) if f.endswith(".cu"))
     jobs = []
     for name, flags in pairs:
         for src in srcs:
