@@ -273,3 +273,17 @@ def test_max_size_64bit_offsets(orc, torch, layout):
         assert np.array_equal(rows(out), want), iters
     del a, b, n, out
     torch.cuda.empty_cache()
+
+
+def test_fault_injection_is_detected(orc, torch):
+    """SURVEY §5 fault injection: one element's modulus corrupted on the device only (a flipped bit,
+    as a corrupted n'_0 would act) is caught by the element-wise parity comparison at exactly that
+    element, and nowhere else — the parity harness has teeth."""
+    L, count = 6, 32 * 9 + 3
+    a, b, n = mulmod_inputs(count, L, seed=77)
+    A, B, Nn = (dev(torch, x) for x in (a, b, n))
+    Nn[17, 2] ^= 1 << 5  # stays odd and in range: a different, valid modulus
+    got = eg.ecm_mulmod_batch(A, B, Nn, L=L, iters=8).cpu().numpy()
+    want = orc.mulmod_chain_mt(a, b, n, L, 8)
+    bad = np.nonzero((got != want).any(axis=1))[0]
+    assert list(bad) == [17]
