@@ -281,8 +281,9 @@ def test_fault_injection_is_detected(orc, torch):
     element, and nowhere else — the parity harness has teeth."""
     L, count = 6, 32 * 9 + 3
     a, b, n = mulmod_inputs(count, L, seed=77)
-    A, B, Nn = (dev(torch, x) for x in (a, b, n))
-    Nn[17, 2] ^= 1 << 5  # stays odd and in range: a different, valid modulus
+    n_dev = n.copy()
+    n_dev[17, 2] ^= np.uint32(1 << 5)  # stays odd and in range: a different, valid modulus
+    A, B, Nn = (dev(torch, x) for x in (a, b, n_dev))
     got = eg.ecm_mulmod_batch(A, B, Nn, L=L, iters=8).cpu().numpy()
     want = orc.mulmod_chain_mt(a, b, n, L, 8)
     bad = np.nonzero((got != want).any(axis=1))[0]
