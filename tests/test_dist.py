@@ -1,4 +1,4 @@
-"""World-size-2 and -3 gloo tests of the multi-GPU shard + gather logic (paper_1310_3809_b200.dist)
+"""World-size-2, -3 and -8 gloo tests of the multi-GPU shard + gather logic (paper_1310_3809_b200.dist)
 on CPU, with the oracle standing in for the per-GPU kernel."""
 import os
 import socket
@@ -48,7 +48,7 @@ def test_shard_bounds_cover_exactly():
             assert all(b[i][1] == b[i + 1][0] for i in range(w - 1))
 
 
-@pytest.mark.parametrize("world", (2, 3))
+@pytest.mark.parametrize("world", (2, 3, 8))
 def test_gloo_gather_equals_single_process(orc, world):
     from workload import ecm_config
     cfg = ecm_config(L=6, nbits=190, pbits=32, B1=300, curves=75, seed=1)  # ragged: 75 curves

@@ -238,3 +238,15 @@ def test_small_family_c3_sampled(orc, torch):
     for i in flagged:
         gi = eg.limbs_to_int(got["g"][i])
         assert 1 < gi < cfg["N"] and cfg["N"] % gi == 0
+
+
+def test_results_independent_of_sharding(torch):
+    """1/2/4/8 contiguous shards (what each rank of an N-GPU run computes)
+    concatenate to the single-launch result, with both kernel choices at the shard sizes."""
+    cfg = ecm_config(L=6, nbits=190, pbits=40, B1=500, curves=3000, seed=61)
+    full = gpu_stage1(torch, cfg["N"], 6, cfg["B1"], cfg["sigmas"])
+    for w in (2, 4, 8):
+        parts = [gpu_stage1(torch, cfg["N"], 6, cfg["B1"], cfg["sigmas"][r * 3000 // w:(r + 1) * 3000 // w])
+                 for r in range(w)]
+        for key in ("X", "Z", "g", "status", "xaff"):
+            assert np.array_equal(np.concatenate([p[key] for p in parts]), full[key]), (w, key)
