@@ -39,6 +39,10 @@ constexpr int kEcmTPB = 128;
 #define ECM_CONST_SMEM 0
 #endif
 //   ECM_LADDER_UNROLL : unroll factor of the one-lane ladder loop
+//   ECM_SQR_CANON   : 1 = the ladder squares canonicalise their input and use the CIOS square
+#ifndef ECM_SQR_CANON
+#define ECM_SQR_CANON 0
+#endif
 #ifndef ECM_LADDER_UNROLL
 #define ECM_LADDER_UNROLL 1
 #endif
@@ -195,7 +199,11 @@ struct Field {
     if (EAGER) canonicalize<L>(r, r, N);
   }
   __device__ __forceinline__ void sqr(uint32_t (&r)[L], const uint32_t (&x)[L]) const {
-    if (V == REDC_WORD) mont_sqr<L>(r, x, N, n0inv);
+    if (V == REDC_WORD && ECM_SQR_CANON) {
+      uint32_t xc[L];
+      canonicalize<L>(xc, x, N);  // x < N: the CIOS square's bound holds
+      mont_sqr_cios<L>(r, xc, N, n0inv);
+    } else if (V == REDC_WORD) mont_sqr<L>(r, x, N, n0inv);
     else if (V == REDC_KNOWNLOW) mont_mul_cios<L, V>(r, x, x, N, n0inv);
     else mont_mul_block<L, V>(r, x, x, N, NP);
     debug_lazy_bound<L>(r, N);

@@ -520,6 +520,86 @@ __device__ __forceinline__ void mont_sqr(uint32_t (&r)[L], const uint32_t (&x)[L
   r[L - 1] = ptx::addc(q[L - 1], T[2 * L - 1]);
 }
 
+// ------------------------------------------------------------------------------------------
+// Row-interleaved (CIOS) Montgomery squaring for a CANONICAL input x < N (ECM ladder only; the
+// mulmod API squares lazy inputs with mont_sqr).  Same unique raw value REDC(x^2) < 2N with
+// (3L^2 + L)/2 partial products and the multiply's per-row carry handling:
+//   x^2 = sum_i x_i V_i 2^(32 i), V_i = x_i + 2 sum_{j>i} x_j 2^(32(j-i)) (words of Y = 2x, bit 0
+//   of Y_{i+1} masked): row i is a CIOS row of x_i times V_i, whose pairs start at word i; rows
+//   i >= 1 leave word 0 alone, so m_i = E_0 n0' is known first and the reduction chain (which
+//   consumes the shift's pending carry) runs before the row's short product chains.
+// Bound: every row adds at most 2^32 (2x + N) before its shift, and with x < N that is
+// < 2^32 3N < (3/4) 2^(32(L+1)) (N < R/4): the odd chains cannot carry out and the even chains'
+// carries fit in O[L-1], as in mont_mul_cios.  (With a lazy x < 2N the sum can reach 2^32 5N,
+// beyond R 2^32 when N is near R/4 — why the lazy square keeps the split form.)
+// ------------------------------------------------------------------------------------------
+template <int L, int PAR, int S, bool COUT>
+__device__ __forceinline__ void chain_from(uint32_t (&d)[L], uint32_t a, const uint32_t (&v)[L]) {
+  constexpr int j0 = (S % 2 == PAR) ? S : S + 1;
+#pragma unroll
+  for (int j = j0; j < L; j += 2) {
+    if (j == j0) d[j - PAR] = ptx::mad_lo_cc(a, v[j], d[j - PAR]);
+    else d[j - PAR] = ptx::madc_lo_cc(a, v[j], d[j - PAR]);
+    if (j + 2 >= L && !COUT) d[j - PAR + 1] = ptx::madc_hi(a, v[j], d[j - PAR + 1]);
+    else d[j - PAR + 1] = ptx::madc_hi_cc(a, v[j], d[j - PAR + 1]);
+  }
+}
+
+template <int L, int I>
+__device__ __forceinline__ void sqr_row_products(uint32_t (&E)[L], uint32_t (&O)[L], const uint32_t (&x)[L],
+                                                 const uint32_t (&Y)[L]) {
+  uint32_t v[L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) v[j] = (j < I) ? 0u : (j == I) ? x[I] : (j == I + 1) ? (Y[j] & 0xfffffffeu) : Y[j];
+  constexpr int je = (I % 2 == 0) ? I : I + 1;  // first even pair
+  constexpr int jo = (I % 2 == 1) ? I : I + 1;  // first odd pair
+  if (jo < L) chain_from<L, 1, jo, false>(O, x[I], v);
+  if (je < L) {
+    chain_from<L, 0, je, true>(E, x[I], v);
+    O[L - 1] = ptx::addc(O[L - 1], 0u);
+  }
+}
+
+template <int L, int I>
+__device__ __forceinline__ void sqr_rows(uint32_t (&E)[L], uint32_t (&O)[L], const uint32_t (&x)[L],
+                                         const uint32_t (&Y)[L], const uint32_t (&n)[L], uint32_t n0inv) {
+  if constexpr (I < L) {
+    if (I == 0) sqr_row_products<L, 0>(E, O, x, Y);
+    const uint32_t m = E[0] * n0inv;
+    chain<L, 1, (I > 0), false>(O, O, m, n);  // rows >= 1: consumes the pending shift carry
+    chain<L, 0, false, true>(E, E, m, n);
+    O[L - 1] = ptx::addc(O[L - 1], 0u);
+    if (I > 0) sqr_row_products<L, I>(E, O, x, Y);
+    uint32_t nE[L], nO[L];
+#pragma unroll
+    for (int k = 0; k < L; ++k) nE[k] = O[k];
+    nE[0] = ptx::add_cc(nE[0], E[1]);
+#pragma unroll
+    for (int k = 0; k < L; ++k) nO[k] = (k + 2 < L) ? E[k + 2] : 0u;
+#pragma unroll
+    for (int k = 0; k < L; ++k) { E[k] = nE[k]; O[k] = nO[k]; }
+    sqr_rows<L, I + 1>(E, O, x, Y, n, n0inv);
+  }
+}
+
+template <int L>
+__device__ __forceinline__ void mont_sqr_cios(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&n)[L],
+                                              uint32_t n0inv) {
+  static_assert(L % 2 == 0 && L >= 2, "L must be even");
+  uint32_t Y[L];
+  Y[0] = x[0] << 1;
+#pragma unroll
+  for (int k = 1; k < L; ++k) Y[k] = __funnelshift_l(x[k - 1], x[k], 1);
+  uint32_t E[L], O[L];
+#pragma unroll
+  for (int k = 0; k < L; ++k) { E[k] = 0; O[k] = 0; }
+  sqr_rows<L, 0>(E, O, x, Y, n, n0inv);
+  r[0] = E[0];  // + O 2^32 + the last shift's pending carry (at word 1)
+#pragma unroll
+  for (int k = 1; k < L - 1; ++k) r[k] = ptx::addc_cc(E[k], O[k - 1]);
+  r[L - 1] = ptx::addc(E[L - 1], O[L - 2]);
+}
+
 // -N^{-1} mod R over the full width, for the block (SOS) REDC variants: Newton lifting
 // x <- x (2 - N x) of N^{-1} from the 32-bit inverse, doubling the correct words.
 template <int L>
