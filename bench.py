@@ -18,6 +18,7 @@ all-gathers the per-curve status bytes over NCCL (strong scaling).
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import subprocess
@@ -317,43 +318,56 @@ def run_ours(args):
     del ah, bh, nh, oh
 
     # ---------------- C3: ECM stage 1 curves/s (strong scaling over ranks) ----------------
-    ecm = None
+    ecm, ecm_last = None, {}
     if not args.no_ecm:
         cfg = ecm_config("C3")
         if args.ecm_b1:
             cfg["B1"] = args.ecm_b1
         curves = cfg["curves"] if args.ecm_curves is None else args.ecm_curves
-        lo, hi = rank * curves // ws, (rank + 1) * curves // ws
-        sig = torch.from_numpy(cfg["sigmas"][lo:hi].copy()).cuda()
         kb = eg.ecm_stage1_kbits(cfg["B1"])
-        eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], sig[:4096], want=("g",))  # warm-up (plan, code)
-        gathered = None
-        ecm_last = {}
+        from paper_1310_3809_b200.dist import ecm_stage1_distributed, shard_bounds
+        gdev = "cuda" if BACKEND == "nccl" else "cpu"  # gloo (tests): the gather runs on CPU tensors
+        sig_all = cfg["sigmas"][:curves]
+        # warm-up: the same distributed step (plan cache, kernels, communicators) on 4096 curves per rank
+        ecm_stage1_distributed(cfg["N"], L, cfg["B1"], sig_all[: 4096 * ws], device=gdev)
+        evs, loc = {}, {}
+        gathered, factors = None, None
 
         def ecm_step():
-            nonlocal gathered
-            if ws > 1:
-                from paper_1310_3809_b200.dist import ecm_stage1_distributed
-                gathered, _ = ecm_stage1_distributed(cfg["N"], L, cfg["B1"], cfg["sigmas"][:curves],
-                                                     device="cuda" if BACKEND == "nccl" else "cpu")
-            else:
-                r = eg.ecm_stage1_batch(cfg["N"], L, cfg["B1"], sig, want=("g",))
-                gathered = r["status"]
-                ecm_last.update(r)
+            nonlocal gathered, factors
+            # shard -> ecm_stage1_batch on this rank's GPU -> status all-gather + factor records
+            # (at N = 1 the same call without collectives)
+            gathered, factors = ecm_stage1_distributed(cfg["N"], L, cfg["B1"], sig_all, device=gdev,
+                                                       events=evs, local=loc)
 
         with ClockSampler(local) as clk2:
             ecm_ms, _ = time_steps(torch, ecm_step, 1, ws)
         ecm_ms = max_over_ranks(torch, ecm_ms, ws)
+        kern_ms = evs["start"].elapsed_time(evs["computed"])
+        gather_ms = evs["computed"].elapsed_time(evs["gathered"])
+        kmax = max_over_ranks(torch, kern_ms, ws)
+        kmin = -max_over_ranks(torch, -kern_ms, ws)
+        gmax = max_over_ranks(torch, gather_ms, ws)
         st = gathered.cpu().numpy()
         curves_s = curves / (ecm_ms * 1e-3)
         fpe_curve = (kb - 1) * FPE_LADDER_STEP
+        lo, hi = shard_bounds(curves, rank, ws)
         ecm = {"workload": f"C3: ECM stage 1, B1={cfg['B1']}, {curves} curves, 190-bit N=p*q (planted 64-bit p)",
                "curves_per_s": curves_s, "modmul_per_s": curves_s * (kb - 1) * MULMODS_PER_STEP,
                "ms": ecm_ms, "k_bits": kb, "flagged_factor": int((st == 1).sum()), "scaling": "strong",
+               "curves_per_rank": [shard_bounds(curves, r, ws)[1] - shard_bounds(curves, r, ws)[0] for r in range(ws)],
+               "kernel_ms_per_rank": {"min": kmin, "max": kmax}, "gather_ms": gmax,
+               "gather_share": gmax / ecm_ms,
+               "status_digest": hashlib.sha256(st.tobytes()).hexdigest()[:16],
                "roofline": {"bound": "alu", "achieved": curves_s / ws * fpe_curve / 1e12,
                             "peak": pk["fpe_peak"] / 1e12, "unit": "Tpp/s",
-                            "frac": curves_s / ws * fpe_curve / pk["fpe_peak"]},
+                            "frac": curves_s / ws * fpe_curve / pk["fpe_peak"],
+                            "frac_kernel": curves / ws / (kmax * 1e-3) * fpe_curve / pk["fpe_peak"]},
                "clocks": clk2.summary()}
+        if rank == 0:
+            ecm["factors_found"] = len(factors)
+            ecm["factors_digest"] = hashlib.sha256(repr(factors).encode()).hexdigest()[:16]
+        ecm_last = {"status": loc["status"], "g": loc["g"]} if ws == 1 else {}
 
     # ---------------- §8(f) N4: the small-parameter family on C3's modulus, B1 and curve count ----------
     if ecm is not None and not args.no_sweep:

@@ -85,14 +85,53 @@ def _count(t, L):
     return n // L
 
 
+def _validate(t, name: str, *, host: bool, dtype: str, numel: int | None = None, shape=None):
+    """Raise ValueError unless `t` is a contiguous array of `dtype` ("uint32" / "uint64" / "uint8")
+    with `numel` elements (and `shape`, if given) that lives where the call expects it: host memory
+    (numpy or a CPU tensor) with ECM_HOST_BUFFERS, else a CUDA tensor on the current device."""
+    if isinstance(t, np.ndarray):
+        if t.dtype != np.dtype(dtype):
+            raise ValueError(f"{name}: dtype {t.dtype}, expected {dtype}")
+        if not host:
+            raise ValueError(f"{name}: host array without ECM_HOST_BUFFERS (a device tensor is required)")
+        n, shp = t.size, tuple(t.shape)
+    else:
+        torch = _torch()
+        if not isinstance(t, torch.Tensor):
+            raise ValueError(f"{name}: expected a torch tensor or numpy array, got {type(t).__name__}")
+        if t.dtype != getattr(torch, dtype):
+            raise ValueError(f"{name}: dtype {t.dtype}, expected torch.{dtype}")
+        if host and t.is_cuda:
+            raise ValueError(f"{name}: CUDA tensor with ECM_HOST_BUFFERS (host memory is required)")
+        if not host:
+            if not t.is_cuda:
+                raise ValueError(f"{name}: CPU tensor without ECM_HOST_BUFFERS (a CUDA tensor is required)")
+            if t.device.index != torch.cuda.current_device():
+                raise ValueError(f"{name}: on {t.device}, but the current device is cuda:{torch.cuda.current_device()}")
+        n, shp = t.numel(), tuple(t.shape)
+    if numel is not None and n != numel:
+        raise ValueError(f"{name}: {n} elements, expected {numel}")
+    if shape is not None and shp != tuple(shape):
+        raise ValueError(f"{name}: shape {shp}, expected {tuple(shape)}")
+
+
 def ecm_mulmod_batch(a, b, n, out=None, *, L: int, iters: int = 1, flags: int = 0, stream=None):
     """out_i = x_iters with x_0 = a_i, x_{t+1} = REDC(x_t * b_i) (or x_t^2 with ECM_SQUARE) mod n_i."""
     count = _count(a, L)
+    host = bool(flags & ECM_HOST_BUFFERS)
+    shape = tuple(a.shape)
+    _validate(a, "a", host=host, dtype="uint32", numel=count * L)
+    if not (flags & ECM_SQUARE):
+        if b is None:
+            raise ValueError("b is required unless ECM_SQUARE")
+        _validate(b, "b", host=host, dtype="uint32", numel=count * L, shape=shape)
+    _validate(n, "n", host=host, dtype="uint32", numel=count * L, shape=shape)
     if out is None:
         if isinstance(a, np.ndarray):
             out = np.empty_like(a)
         else:
             out = _torch().empty_like(a)
+    _validate(out, "out", host=host, dtype="uint32", numel=count * L, shape=shape)
     st = lib().ecm_mulmod_batch(_ptr(a), _ptr(b), _ptr(n), _ptr(out), count, L, iters, flags, _stream(stream))
     _check(st, "ecm_mulmod_batch")
     return out
@@ -108,7 +147,8 @@ def _alloc(like_host: bool, shape, dtype_np, device=None):
 
 def _run_curves(fn, N, L, args, sigmas, flags, stream, want):
     host = bool(flags & ECM_HOST_BUFFERS)
-    count = sigmas.numel() if hasattr(sigmas, "numel") else np.asarray(sigmas).size
+    _validate(sigmas, "sigmas", host=host, dtype="uint64")
+    count = sigmas.numel() if hasattr(sigmas, "numel") else sigmas.size
     Nl = int_to_limbs(int(N), L)
     dev = None if host else sigmas.device
     outs = {k: (_alloc(host, (count, L), np.uint32, dev) if k in want else None) for k in ("X", "Z", "g", "xaff")}

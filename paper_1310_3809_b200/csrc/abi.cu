@@ -355,13 +355,16 @@ ecm_status ecm_mulmod_batch(const uint32_t* a, const uint32_t* b, const uint32_t
   if (host && !(flags & ECM_CHECK))
     return cuda_err(mulmod_host_pipelined(a, b, n, out, count, L, iters, flags, s));
   if (host) {
-    e = dev_alloc(&scratch, 4 * bytes + 16, s);
+    // four sub-buffers, each starting on a 16-byte boundary (the AoS kernels move tiles with bulk
+    // copies and 128-bit accesses, which need it): stride rounded up to a multiple of 4 words
+    const size_t stride = (count * (size_t)L + 3) & ~(size_t)3;
+    e = dev_alloc(&scratch, 4 * stride * sizeof(uint32_t), s);
     if (e != cudaSuccess) return cuda_err(e);
     uint32_t* base = reinterpret_cast<uint32_t*>(scratch);
     uint32_t* ta = base;
-    uint32_t* tb = base + count * L;
-    uint32_t* tn = base + 2 * count * L;
-    dout = base + 3 * count * L;
+    uint32_t* tb = base + stride;
+    uint32_t* tn = base + 2 * stride;
+    dout = base + 3 * stride;
     e = cudaMemcpyAsync(ta, a, bytes, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && !square) e = cudaMemcpyAsync(tb, b, bytes, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(tn, n, bytes, cudaMemcpyHostToDevice, s);

@@ -34,6 +34,18 @@ constexpr int kEcmTPB = 128;
 #ifndef ECM_SWAP_BRANCH
 #define ECM_SWAP_BRANCH 0
 #endif
+//   ECM_SWAP_SEL    : 1 (default) = no state swap; the doubling's input sums are selected
+//                     (ladder_step_sel, 2L instead of 4L selects per step); 0 = conditional swap
+#ifndef ECM_SWAP_SEL
+#define ECM_SWAP_SEL 1
+#endif
+//   ECM_LADDER_SQR  : square form in the ladder (mont_sqr FORM; -1 = per-width default below)
+#ifndef ECM_LADDER_SQR
+#define ECM_LADDER_SQR -1
+#endif
+// L = 6 keeps the merged square in the ladder: with the unmerged form the 80-register ladder spills
+// more (profiles/r02a_ab6.jsonl); every other width takes the unmerged form.
+__host__ __device__ constexpr int ladder_sqr_form(int L) { return ECM_LADDER_SQR >= 0 ? ECM_LADDER_SQR : L == 6 ? 0 : 1; }
 //   ECM_CONST_SMEM  : 1 = x0 and a24 live in shared memory during the ladder (loaded per use)
 #ifndef ECM_CONST_SMEM
 #define ECM_CONST_SMEM 0
@@ -146,12 +158,16 @@ __device__ __forceinline__ void sub_modN(uint32_t (&d)[L], const uint32_t (&a)[L
   d[L - 1] = ptx::addc(t[L - 1], N[L - 1] & mask);
 }
 
-// Binary extended gcd ("right-shift" form, v kept odd):
-//   u = a, v = N, A = 1, C = 0 with A a = u, C a = v (mod N);
-//   while u != 0: strip factors 2 from u (halving A mod N); if u < v swap (u,A) <-> (v,C);
-//   u -= v, A -= C.   On exit v = gcd(a, N) and, if v == 1, C = a^{-1} mod N.
-// a < N canonical, N odd.  Returns true iff invertible.  Data-dependent trip count (setup and
-// tail only: < 0.5% of a curve at the smallest B1).
+// Constant-iteration binary extended gcd, no data-dependent branch (PAPER.md:152-154 asks SIMD
+// code to avoid them; the lanes of a warp hold different curves):
+//   u = a, v = N (odd), A = 1, C = 0 with A a = u, C a = v (mod N).  Each iteration
+//     if u odd:  if u < v: (u, A) <-> (v, C);  u -= v;  A -= C (mod N)       [masks and selects]
+//     u /= 2;  A /= 2 (mod N)
+//   keeps v odd.  While u != 0 every iteration lowers bitlen(u) + bitlen(v) (<= 2 bitlen(N)
+//   initially, >= 2 while u != 0) by at least one, so after 64L - 4 >= 2(32L - 2) iterations
+//   u = 0; from then on v and C no longer change: v = gcd(a, N) and, if v = 1, C = a^{-1} mod N.
+// a < N canonical (a = 0 gives g = N).  Returns true iff invertible.  The trip count is the same
+// for every lane (setup and tail only).
 template <int L>
 __device__ bool xgcd(const uint32_t (&a)[L], const uint32_t (&N)[L], uint32_t (&g)[L], uint32_t (&inv)[L]) {
   uint32_t u[L], v[L], A[L], C[L];
@@ -160,24 +176,48 @@ __device__ bool xgcd(const uint32_t (&a)[L], const uint32_t (&N)[L], uint32_t (&
 #pragma unroll
   for (int k = 0; k < L; ++k) { A[k] = 0; C[k] = 0; }
   A[0] = 1;
-  while (!is_zero(u)) {
-    while (!(u[0] & 1u)) {
-      shr1(u);
-      half_mod(A, N);
-    }
-    if (!geq(u, v)) {
+#pragma unroll 1
+  for (int it = 0; it < 64 * L - 4; ++it) {
+    const uint32_t odd = 0u - (u[0] & 1u);
+    (void)ptx::sub_cc(u[0], v[0]);
 #pragma unroll
-      for (int k = 0; k < L; ++k) {
-        uint32_t t = u[k]; u[k] = v[k]; v[k] = t;
-        t = A[k]; A[k] = C[k]; C[k] = t;
-      }
+    for (int k = 1; k < L; ++k) (void)ptx::subc_cc(u[k], v[k]);
+    const uint32_t sw = odd & ptx::subc(0u, 0u);  // u odd and u < v
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+      const uint32_t du = (u[k] ^ v[k]) & sw, dA = (A[k] ^ C[k]) & sw;
+      u[k] ^= du;
+      v[k] ^= du;
+      A[k] ^= dA;
+      C[k] ^= dA;
     }
-    sub_plain(u, u, v);
-    sub_modN(A, A, C, N);
+    // u -= v (u >= v now), A -= C (mod N): both only when u was odd
+    u[0] = ptx::sub_cc(u[0], v[0] & odd);
+#pragma unroll
+    for (int k = 1; k < L - 1; ++k) u[k] = ptx::subc_cc(u[k], v[k] & odd);
+    u[L - 1] = ptx::subc(u[L - 1], v[L - 1] & odd);
+    uint32_t t[L];
+    t[0] = ptx::sub_cc(A[0], C[0] & odd);
+#pragma unroll
+    for (int k = 1; k < L; ++k) t[k] = ptx::subc_cc(A[k], C[k] & odd);
+    const uint32_t br = ptx::subc(0u, 0u);
+    A[0] = ptx::add_cc(t[0], N[0] & br);
+#pragma unroll
+    for (int k = 1; k < L - 1; ++k) A[k] = ptx::addc_cc(t[k], N[k] & br);
+    A[L - 1] = ptx::addc(t[L - 1], N[L - 1] & br);
+    shr1(u);
+    half_mod(A, N);
   }
   copy(g, v);
   copy(inv, C);
   return is_one(v);
+}
+
+// d = m ? a : b for an all-ones / zero mask m
+template <int L>
+__device__ __forceinline__ void select(uint32_t (&d)[L], uint32_t m, const uint32_t (&a)[L], const uint32_t (&b)[L]) {
+#pragma unroll
+  for (int k = 0; k < L; ++k) d[k] = (a[k] & m) | (b[k] & ~m);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -203,7 +243,7 @@ struct Field {
       uint32_t xc[L];
       canonicalize<L>(xc, x, N);  // x < N: the CIOS square's bound holds
       mont_sqr_cios<L>(r, xc, N, n0inv);
-    } else if (V == REDC_WORD) mont_sqr<L>(r, x, N, n0inv);
+    } else if (V == REDC_WORD) mont_sqr<L, ladder_sqr_form(L)>(r, x, N, n0inv);
     else if (V == REDC_KNOWNLOW) mont_mul_cios<L, V>(r, x, x, N, n0inv);
     else mont_mul_block<L, V>(r, x, x, N, NP);
     debug_lazy_bound<L>(r, N);
@@ -235,6 +275,42 @@ __device__ __forceinline__ void ladder_step(uint32_t (&X0)[L], uint32_t (&Z0)[L]
   f.sub(t4, X1, Z1);
   f.mul(U, t2, t3);
   f.mul(V, t1, t4);
+  f.sqr(s, t1);
+  f.sqr(d, t2);
+  f.mul(X0, s, d);
+  f.sub(t1, s, d);   // t
+  f.mul(t2, a24, t1); // a24 t
+  f.add(t2, d, t2);  // d + a24 t
+  f.mul(Z0, t1, t2);
+  f.add(t3, U, V);
+  f.sub(t4, U, V);
+  f.sqr(X1, t3);
+  f.sqr(t4, t4);
+  f.mul(Z1, x0, t4);
+}
+
+// The same step without a state swap: the slots are not exchanged; `c` picks which slot's sums
+// (t1, t2) or (t3, t4) feed the doubling.  The addition is symmetric in its two inputs — swapping
+// the slots exchanges U and V, leaves U + V and flips the sign of U - V, which is squared — so the
+// doubled point always lands in slot 0 and the sum in slot 1: 2L selects per step instead of the
+// 4L of a conditional swap of (X0:Z0) and (X1:Z1).  Every product is congruent mod N to the one
+// ladder_step computes, so the canonical outputs are identical.
+template <int L, class F>
+__device__ __forceinline__ void ladder_step_sel(uint32_t (&X0)[L], uint32_t (&Z0)[L], uint32_t (&X1)[L],
+                                                uint32_t (&Z1)[L], const uint32_t (&x0)[L], const uint32_t (&a24)[L],
+                                                const F& f, bool c) {
+  uint32_t t1[L], t2[L], t3[L], t4[L], U[L], V[L], s[L], d[L];
+  f.add(t1, X0, Z0);
+  f.sub(t2, X0, Z0);
+  f.add(t3, X1, Z1);
+  f.sub(t4, X1, Z1);
+  f.mul(U, t2, t3);
+  f.mul(V, t1, t4);
+#pragma unroll
+  for (int k = 0; k < L; ++k) {
+    t1[k] = c ? t3[k] : t1[k];
+    t2[k] = c ? t4[k] : t2[k];
+  }
   f.sqr(s, t1);
   f.sqr(d, t2);
   f.mul(X0, s, d);
@@ -369,12 +445,14 @@ __device__ __forceinline__ void cswap(uint32_t (&a)[L], uint32_t (&b)[L], bool c
   }
 }
 
+// curve i's L words when `on` (a predicated store; dst == nullptr: not wanted, kernel-uniform)
 template <int L>
-__device__ __forceinline__ void store(uint32_t* dst, size_t i, const uint32_t (&v)[L]) {
+__device__ __forceinline__ void store_if(uint32_t* dst, size_t i, const uint32_t (&v)[L], bool on) {
   if (!dst) return;
   uint2* d2 = reinterpret_cast<uint2*>(dst + i * L);
 #pragma unroll
-  for (int k = 0; k < L / 2; ++k) d2[k] = make_uint2(v[2 * k], v[2 * k + 1]);
+  for (int k = 0; k < L / 2; ++k)
+    if (on) d2[k] = make_uint2(v[2 * k], v[2 * k + 1]);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -423,32 +501,29 @@ __device__ __forceinline__ uint8_t ecm_setup(const EcmParams& p, uint64_t sigma,
   mont_mul<L>(Dn, D, c, N, n0inv);
   canonicalize<L>(Dn, Dn, N);
   const bool ok = xgcd<L>(Dn, N, gg, Di);
-  uint8_t st;
-  if (ok) {
-    mont_mul<L>(w, Di, R2, N, n0inv);              // w = D^{-1} (Montgomery form)
-    // x0 = 16 u^3 * u^3 * v * w
-    mont_mul<L>(c, t, u3, N, n0inv);
-    mont_mul<L>(c, c, v, N, n0inv);
-    mont_mul<L>(x0, c, w, N, n0inv);
-    // a24 = (v-u)^3 (3u+v) v^3 w
-    sub_lazy<L>(t, v, u, N2);
-    mont_mul<L>(c, t, t, N, n0inv);
-    mont_mul<L>(c, c, t, N, n0inv);
-    mont_mul<L>(t, three, u, N, n0inv);
-    add_lazy<L>(t, t, v, N2);
-    mont_mul<L>(c, c, t, N, n0inv);
-    mont_mul<L>(c, c, v3, N, n0inv);
-    mont_mul<L>(a24, c, w, N, n0inv);
-    st = 0;
-  } else {
-    // gcd(D, N) == N (D == 0 mod N) -> 3; proper factor -> 4
-    st = equal(gg, N) ? 3 : 4;
+  // both outcomes are computed and selected (no divergent branch): with D not invertible the
+  // curve's (x0, a24) = (1, 0) keep the discarded ladder arithmetic well-defined
+  mont_mul<L>(w, Di, R2, N, n0inv);                // w = D^{-1} (Montgomery form)
+  // x0 = 16 u^3 * u^3 * v * w
+  mont_mul<L>(c, t, u3, N, n0inv);
+  mont_mul<L>(c, c, v, N, n0inv);
+  mont_mul<L>(x0, c, w, N, n0inv);
+  // a24 = (v-u)^3 (3u+v) v^3 w
+  sub_lazy<L>(t, v, u, N2);
+  mont_mul<L>(c, t, t, N, n0inv);
+  mont_mul<L>(c, c, t, N, n0inv);
+  mont_mul<L>(t, three, u, N, n0inv);
+  add_lazy<L>(t, t, v, N2);
+  mont_mul<L>(c, c, t, N, n0inv);
+  mont_mul<L>(c, c, v3, N, n0inv);
+  mont_mul<L>(a24, c, w, N, n0inv);
+  const uint32_t okm = 0u - (uint32_t)ok;
+  select<L>(x0, okm, x0, ONE);
 #pragma unroll
-    for (int k = 0; k < L; ++k) { x0[k] = 0; a24[k] = 0; }
-    copy(x0, ONE);  // keep the (discarded) ladder arithmetic well-defined
-  }
-
-  return st;
+  for (int k = 0; k < L; ++k) a24[k] &= okm;
+  // gcd(D, N) == N (D == 0 mod N) -> 3; proper factor -> 4 (both tests evaluated: no branch)
+  const uint32_t eqN = equal(gg, N), okv = ok;
+  return (uint8_t)((1u - okv) * (4u - eqN));
 }
 
 // Small-parameter family (reading G16 — not the paper's curves): a
@@ -479,55 +554,57 @@ __device__ __forceinline__ uint8_t ecm_setup_store(const EcmParams& p, uint64_t 
   } else {
     st = ecm_setup<L>(p, sigma, x0, a24, gg);
   }
-  if (live && st != 0) store<L>(g, i, gg);
+  store_if<L>(g, i, gg, live && st != 0);
   return st;
 }
 
 // ---------------------------------------------------------------------------------------
 // Tail: X, Z out of Montgomery form and canonical; g = gcd(Z, N) and Z^{-1} by one binary xgcd;
-// status; affine x = X Z^{-1}.  Writes curve i's outputs.
+// status; affine x = X Z^{-1}.  Writes curve i's outputs (dead lanes compute and
+// store nothing).  Branch-free: the gcd and the affine x are computed for every curve and the
+// outputs selected by status.
 // ---------------------------------------------------------------------------------------
 // A curve whose setup failed (st = 3 / 4) had its g written by ecm_setup_store already, so the
 // setup gcd is not live across the ladder.
 template <int L>
 __device__ __forceinline__ void ecm_tail(const EcmParams& p, const uint32_t (&X0)[L], const uint32_t (&Z0)[L], uint8_t st,
-                                         size_t i, uint32_t* X, uint32_t* Z, uint32_t* g,
+                                         bool live, size_t i, uint32_t* X, uint32_t* Z, uint32_t* g,
                                          uint8_t* status, uint32_t* xaff, uint32_t flags) {
-  uint32_t gg[L];
+  uint32_t gg[L], Zi[L];
   const uint32_t(&N)[L] = cref<L>(p.N);
   const uint32_t(&R2)[L] = cref<L>(p.R2);
   const uint32_t n0inv = p.n0inv;
   uint32_t c[L], t[L];
   uint32_t Xn[L], Zn[L], xa[L];
 #pragma unroll
-  for (int k = 0; k < L; ++k) { c[k] = 0; xa[k] = 0; }
+  for (int k = 0; k < L; ++k) c[k] = 0;
   c[0] = 1;
   mont_mul<L>(Xn, X0, c, N, n0inv);
   canonicalize<L>(Xn, Xn, N);
   mont_mul<L>(Zn, Z0, c, N, n0inv);
   canonicalize<L>(Zn, Zn, N);
-  if (st == 0) {
-    uint32_t Zi[L];
-    const bool inv = xgcd<L>(Zn, N, gg, Zi);
-    if (inv) {
-      st = 0;
-      if (xaff && !(flags & 0x20u)) {
-        mont_mul<L>(t, Xn, R2, N, n0inv);      // X R
-        mont_mul<L>(xa, t, Zi, N, n0inv);      // X Z^{-1}
-        canonicalize<L>(xa, xa, N);
-      }
-    } else {
-      st = equal(gg, N) ? 2 : 1;
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < L; ++k) { Xn[k] = 0; Zn[k] = 0; }
+  const bool inv = xgcd<L>(Zn, N, gg, Zi);
+  const bool want_x = xaff && !(flags & 0x20u);  // kernel-uniform
+  if (want_x) {
+    mont_mul<L>(t, Xn, R2, N, n0inv);  // X R
+    mont_mul<L>(xa, t, Zi, N, n0inv);  // X Z^{-1}
+    canonicalize<L>(xa, xa, N);
   }
-  store<L>(X, i, Xn);
-  store<L>(Z, i, Zn);
-  if (st <= 2) store<L>(g, i, gg);
-  if (xaff && !(flags & 0x20u)) store<L>(xaff, i, xa);
-  status[i] = st;
+  // status: the setup's (3 / 4) if it failed, else 0 (Z invertible), 2 (g = N) or 1 (proper factor)
+  const uint32_t eqN = equal(gg, N), invv = inv, stv = st;
+  const uint8_t so = (uint8_t)(stv + (stv == 0u) * (1u - invv) * (1u + eqN));
+  const uint32_t keep = 0u - (uint32_t)(st == 0), xkeep = 0u - (uint32_t)(so == 0);
+#pragma unroll
+  for (int k = 0; k < L; ++k) {
+    Xn[k] &= keep;
+    Zn[k] &= keep;
+    xa[k] &= xkeep;
+  }
+  store_if<L>(X, i, Xn, live);
+  store_if<L>(Z, i, Zn, live);
+  store_if<L>(g, i, gg, live && so <= 2);
+  if (want_x) store_if<L>(xaff, i, xa, live);
+  if (live) status[i] = so;
 }
 
 template <int L, int VAR, bool EAGER, bool PRIMES, int FAM>
@@ -583,6 +660,16 @@ __global__ void __launch_bounds__(kEcmTPB, ecm_min_blocks(L, VAR, EAGER, PRIMES)
         // bit is warp-uniform, so this is a uniform branch between two copies of the step.
         if (bit) ladder_step<L>(X1, Z1, X0, Z0, x0, a24, fld);
         else ladder_step<L>(X0, Z0, X1, Z1, x0, a24, fld);
+#elif ECM_SWAP_SEL
+        // slot 0 holds R_swapped: double slot (bit != swapped), write the double to slot 0
+        if (FAM == 1) {
+          cswap<L>(X0, X1, bit != swapped);
+          cswap<L>(Z0, Z1, bit != swapped);
+          ladder_step_small<L>(X0, Z0, X1, Z1, cs, N, n0inv, fld);
+        } else {
+          ladder_step_sel<L>(X0, Z0, X1, Z1, x0, a24, fld, bit != swapped);
+        }
+        swapped = bit;
 #else
         // bit 1: (R0, R1) <- (xADD, xDBL(R1)); bit 0: (xDBL(R0), xADD).  Double the point in the
         // (X0,Z0) slot: swap so that slot holds R_bit, swap back lazily on the next change.
@@ -630,8 +717,7 @@ __global__ void __launch_bounds__(kEcmTPB, ecm_min_blocks(L, VAR, EAGER, PRIMES)
     }
   }
 
-  if (!live) return;
-  ecm_tail<L>(p, X0, Z0, st, i, X, Z, g, status, xaff, flags);
+  ecm_tail<L>(p, X0, Z0, st, live, i, X, Z, g, status, xaff, flags);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -758,8 +844,7 @@ __global__ void __launch_bounds__(kCoopTPB) ecm_stage1_coop_kernel(const __grid_
   }
   cswap<L>(X0, X1, swapped);
   cswap<L>(Z0, Z1, swapped);
-  if (!live || q != 0) return;
-  ecm_tail<L>(p, X0, Z0, st, i, X, Z, g, status, xaff, flags);
+  ecm_tail<L>(p, X0, Z0, st, live && q == 0, i, X, Z, g, status, xaff, flags);
 }
 
 // Batches up to this many curves per SM take the 4-lane kernel by default: below ~80 curves/SM

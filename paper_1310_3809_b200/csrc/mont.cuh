@@ -437,7 +437,11 @@ __device__ __forceinline__ void mont_mul_kara(uint32_t (&r)[L], const uint32_t (
 //   only earlier carries and is absorbed by one add, never rippled.
 //   Reduction: the even/odd CIOS frame of mont_mul_cios on T mod R, plus T's high half.
 // ------------------------------------------------------------------------------------------
-template <int L>
+//   FORM 1 (default): the triangle's even/odd accumulators are not merged — their low halves enter
+//   the reduction frame directly and their high halves are added at the end (5 fewer additions at
+//   L = 6; measured +2.3 % in square mode at L = 4 and 6, profiles/r02a_ab*.jsonl).  FORM 0: T is
+//   merged first.  Both give the same raw value.
+template <int L, int FORM = 1>
 __device__ __forceinline__ void mont_sqr(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&n)[L], uint32_t n0inv) {
   static_assert(L % 2 == 0 && L >= 2, "L must be even");
   uint32_t Y[L];
@@ -478,6 +482,47 @@ __device__ __forceinline__ void mont_sqr(uint32_t (&r)[L], const uint32_t (&x)[L
       const int w = 2 * row + klast + 2;
       OD[w] = ptx::addc(OD[w], 0u);
     }
+  }
+  if constexpr (FORM == 1) {
+  // T = A + B R with A = EV mod R + OD mod R (< 2R, not merged) and B = EV div R + OD div R.
+  // q depends only on A mod R = T mod R, so REDC(T) = (A + qN)/R + B.  The frame starts from
+  // E = EV[0..L), O = OD[1..L) (O[k] has weight k+1; OD[0] = 0), O[L-1] = 0: its running value
+  // stays < 2R + 2^32 N < (3/4) 2^(32(L+1)), so the chains' carry bounds of mont_mul_cios hold.
+  {
+    uint32_t E[L], O[L];
+#pragma unroll
+    for (int k = 0; k < L; ++k) { E[k] = EV[k]; O[k] = (k + 1 < L) ? OD[k + 1] : 0u; }
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      const uint32_t m = E[0] * n0inv;
+      if (i == 0) chain<L, 1, false, false>(O, O, m, n);
+      else chain<L, 1, true, false>(O, O, m, n);
+      chain<L, 0, false, true>(E, E, m, n);
+      O[L - 1] = ptx::addc(O[L - 1], 0u);
+      uint32_t nE[L], nO[L];
+#pragma unroll
+      for (int k = 0; k < L; ++k) nE[k] = O[k];
+      nE[0] = ptx::add_cc(nE[0], E[1]);
+#pragma unroll
+      for (int k = 0; k < L; ++k) nO[k] = (k + 2 < L) ? E[k + 2] : 0u;
+#pragma unroll
+      for (int k = 0; k < L; ++k) { E[k] = nE[k]; O[k] = nO[k]; }
+    }
+    uint32_t q[L];
+    q[0] = E[0];
+#pragma unroll
+    for (int k = 1; k < L - 1; ++k) q[k] = ptx::addc_cc(E[k], O[k - 1]);
+    q[L - 1] = ptx::addc(E[L - 1], O[L - 2]);
+    q[0] = ptx::add_cc(q[0], EV[L]);
+#pragma unroll
+    for (int k = 1; k < L - 1; ++k) q[k] = ptx::addc_cc(q[k], EV[L + k]);
+    q[L - 1] = ptx::addc(q[L - 1], EV[2 * L - 1]);
+    r[0] = ptx::add_cc(q[0], OD[L]);
+#pragma unroll
+    for (int k = 1; k < L - 1; ++k) r[k] = ptx::addc_cc(q[k], OD[L + k]);
+    r[L - 1] = ptx::addc(q[L - 1], OD[2 * L - 1]);
+    return;
+  }
   }
   // T = EV + OD (< 2^(64L): the top carry and EV/OD[2L] are zero)
   uint32_t T[2 * L];

@@ -28,7 +28,10 @@ __global__ void mulmod_check_kernel(const uint32_t* __restrict__ a, const uint32
       nn[k] = n[off];
     }
     uint32_t code = 0;
-    if (!(nn[0] & 1u) || (L == 1 && nn[0] < 3)) code = 2;  // ECM_E_MODULUS
+    uint32_t upper = 0;
+#pragma unroll
+    for (int k = 1; k < L; ++k) upper |= nn[k];
+    if (!(nn[0] & 1u) || (upper == 0 && nn[0] < 3)) code = 2;  // ECM_E_MODULUS: even, or N = 1
     else if (nn[L - 1] >> 30) code = 3;                    // ECM_E_WIDTH
     else {
       // 2n (fits L words since n < 2^(32L-2))
@@ -53,6 +56,10 @@ __global__ void mulmod_check_kernel(const uint32_t* __restrict__ a, const uint32
 
 cudaError_t launch_mulmod(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out, size_t count,
                           int L, uint32_t iters, uint32_t flags, cudaStream_t s, size_t* wave) {
+#ifdef ECM_ONLY_L  // single-width build (tools/ecm_ab.py variant libraries)
+  if (L == ECM_ONLY_L) return launch_mulmod_L<ECM_ONLY_L>(a, b, n, out, count, iters, flags, s, wave);
+  return cudaErrorInvalidValue;
+#endif
   switch (L) {
     case 6: return launch_mulmod_L<6>(a, b, n, out, count, iters, flags, s, wave);
     case 4: return launch_mulmod_L<4>(a, b, n, out, count, iters, flags, s, wave);

@@ -23,6 +23,10 @@
 namespace ecm {
 
 constexpr int kMulmodTPB = 256;
+// Internal flag (never accepted from callers: abi.cu rejects unknown bits before it is set): every
+// limb-sliced row is 16-byte aligned — count % 4 == 0 and a, b, n, out 16-byte aligned — so the
+// warp-tile kernel may move sliced tiles with 128-bit accesses.
+constexpr uint32_t kVec16 = 1u << 30;
 // Occupancy floor for the headline kernels (AoS, word-serial REDC, L <= 6): 6 CTAs x 8 warps per
 // SM needs <= 40 registers, which the hot loop fits; other instantiations are left unconstrained.
 // Chain-loop unroll and the limb-sliced L <= 6 kernels' occupancy (tools/ecm_ab.py variants,
@@ -110,13 +114,14 @@ __device__ __forceinline__ void load_aos(uint32_t (&v)[L], const uint32_t* __res
 }
 
 // Limb-sliced tile (ECM_LAYOUT_SLICED): limb j of the warp's 32 elements is the 128-byte row
-// g[j*count + e0 .. +32).  With 16-byte-aligned rows (count % 4 == 0) the warp moves the L rows
-// with 128-bit loads, 8 lanes per row, into smem tile[j*32 + lane]; each lane then reads its
-// limb j at tile[j*32 + lane] (consecutive lanes, consecutive banks: conflict-free).
+// g[j*count + e0 .. +32).  With 16-byte-aligned rows (`vec`: count % 4 == 0 and every array
+// 16-byte aligned, decided on the host: kVec16) the warp moves the L rows with 128-bit loads, 8
+// lanes per row, into smem tile[j*32 + lane]; each lane then reads its limb j at tile[j*32 + lane]
+// (consecutive lanes, consecutive banks: conflict-free).  Otherwise 32-bit loads.
 template <int L>
 __device__ __forceinline__ void load_sliced(uint32_t (&v)[L], const uint32_t* __restrict__ g, uint32_t* tile,
-                                            size_t count, size_t e0, int nvalid, int lane) {
-  if (nvalid == 32 && (count & 3) == 0) {
+                                            size_t count, size_t e0, int nvalid, int lane, bool vec) {
+  if (nvalid == 32 && vec) {
     uint4* t4 = reinterpret_cast<uint4*>(tile);
 #pragma unroll
     for (int k = lane; k < 8 * L; k += 32) {
@@ -135,8 +140,8 @@ __device__ __forceinline__ void load_sliced(uint32_t (&v)[L], const uint32_t* __
 
 template <int L>
 __device__ __forceinline__ void store_sliced(uint32_t* __restrict__ g, const uint32_t (&v)[L], uint32_t* tile,
-                                             size_t count, size_t e0, int nvalid, int lane) {
-  if (nvalid == 32 && (count & 3) == 0) {
+                                             size_t count, size_t e0, int nvalid, int lane, bool vec) {
+  if (nvalid == 32 && vec) {
 #pragma unroll
     for (int j = 0; j < L; ++j) tile[j * 32 + lane] = v[j];
     __syncwarp();
@@ -231,6 +236,7 @@ __global__ void __launch_bounds__(kMulmodTPB, mulmod_min_blocks(L, V, SLICED)) m
   uint32_t* tN = tB + TW;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (kMulmodTPB / 32) * 3 * TW) + warp;
   const bool canon = flags & 0x1u;
+  const bool vec = flags & kVec16;
   // bulk-copy path: AoS full tiles (one 32*L-word copy per array).  Limb-sliced tiles would need
   // L 128-byte copies per array: measured slower than 128-bit loads (48.7 % vs 55.8 % of HBM at
   // K = 1), and so was issuing all three arrays' 128-bit loads before one sync (51 %, 94
@@ -266,9 +272,9 @@ __global__ void __launch_bounds__(kMulmodTPB, mulmod_min_blocks(L, V, SLICED)) m
         nn[k] = tN[idx];
       }
     } else if (SLICED) {
-      load_sliced<L>(x, a, tA, count, e0, nvalid, lane);
-      if (!SQUARE) load_sliced<L>(y, b, tA, count, e0, nvalid, lane);
-      load_sliced<L>(nn, n, tA, count, e0, nvalid, lane);
+      load_sliced<L>(x, a, tA, count, e0, nvalid, lane, vec);
+      if (!SQUARE) load_sliced<L>(y, b, tA, count, e0, nvalid, lane, vec);
+      load_sliced<L>(nn, n, tA, count, e0, nvalid, lane, vec);
     } else {
       load_aos<L>(x, a, tA, e0, nvalid, lane);
       if (!SQUARE) load_aos<L>(y, b, tA, e0, nvalid, lane);
@@ -288,7 +294,7 @@ __global__ void __launch_bounds__(kMulmodTPB, mulmod_min_blocks(L, V, SLICED)) m
         bulk_commit();
       }
     } else if (SLICED) {
-      store_sliced<L>(out, x, tA, count, e0, nvalid, lane);
+      store_sliced<L>(out, x, tA, count, e0, nvalid, lane, vec);
     } else {
       store_aos<L>(out, x, tA, e0, nvalid, lane);
     }
@@ -462,6 +468,11 @@ static cudaError_t launch_mulmod_LV(const uint32_t* a, const uint32_t* b, const 
   if (blocks > 0x7fffffffull) blocks = 0x7fffffffull;
   const unsigned g = (unsigned)blocks;
   const bool sq = flags & 0x2u, sl = flags & 0x4u;
+  {
+    const auto al = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+    flags &= ~kVec16;
+    if (sl && (count & 3u) == 0 && al(a) && al(b) && al(n) && al(out)) flags |= kVec16;
+  }
   constexpr size_t smem = (size_t)(kMulmodTPB / 32) * (3 * 32 * L * sizeof(uint32_t) + sizeof(uint64_t));
   static_assert(smem <= 200 * 1024, "tile staging does not fit shared memory");
   auto sm_count = [](int* sms) -> cudaError_t {

@@ -29,15 +29,37 @@ def _oracle_compute(N, L, B1, sig_t):
     return {"status": torch.from_numpy(r["status"]), "g": torch.from_numpy(r["g"].astype(np.int64))}
 
 
-def _worker(rank, world, port, cfg, out_q):
+def _worker(rank, world, port, cfg, out_q, capacity=None, decode="rank0"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         status, factors = ecm_stage1_distributed(cfg["N"], cfg["L"], cfg["B1"], cfg["sigmas"],
-                                                 compute=_oracle_compute, device="cpu")
+                                                 compute=_oracle_compute, device="cpu", capacity=capacity,
+                                                 decode=decode)
         out_q.put((rank, status.numpy().tobytes(), factors))
     finally:
         dist.destroy_process_group()
+
+
+def _run_world(world, cfg, **kw):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q), kwargs=kw) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return sorted(results, key=lambda r: r[0])
+
+
+def _want(orc, cfg):
+    k, _ = orc.stage1_k(cfg["B1"])
+    want = orc.ecm_stage1(cfg["N"], 6, k, cfg["sigmas"])
+    fl = np.nonzero((want["status"] == 1) | (want["status"] == 4))[0]
+    return want, sorted((int(i), orc.from_limbs(want["g"][i])) for i in fl)
 
 
 def test_shard_bounds_cover_exactly():
@@ -53,21 +75,57 @@ def test_gloo_gather_equals_single_process(orc, world):
     from workload import ecm_config
     cfg = ecm_config(L=6, nbits=190, pbits=32, B1=300, curves=75, seed=1)  # ragged: 75 curves
     cfg = {k: cfg[k] for k in ("N", "L", "B1", "sigmas")}
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    results = [q.get(timeout=300) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    k, _ = orc.stage1_k(cfg["B1"])
-    want = orc.ecm_stage1(cfg["N"], 6, k, cfg["sigmas"])
-    want_factors = sorted((int(i), orc.from_limbs(want["g"][i])) for i in np.nonzero(want["status"] == 1)[0])
+    results = _run_world(world, cfg)
+    want, want_factors = _want(orc, cfg)
     for rank, st_bytes, factors in results:
         st = np.frombuffer(st_bytes, np.uint8)
         assert np.array_equal(st, want["status"]), rank
-        assert factors == want_factors, rank
+        # rank 0 decodes the gathered records; the other ranks only hold the tensors
+        assert factors == (want_factors if rank == 0 else None), rank
     assert len(want_factors) > 0
+
+
+def test_gloo_capacity_overflow_regathers(orc):
+    """A rank with more factor-finding curves than the fixed capacity triggers the exact second
+    gather after the first pair of collectives; every rank decodes the same list (decode="all")."""
+    from workload import ecm_config
+    cfg = ecm_config("C1")  # B1 = 2000: about 10 % of the curves find the planted 32-bit p
+    cfg = {"N": cfg["N"], "L": 6, "B1": cfg["B1"], "sigmas": cfg["sigmas"][:64]}
+    results = _run_world(2, cfg, capacity=1, decode="all")
+    want, want_factors = _want(orc, cfg)
+    assert len(want_factors) >= 4
+    for rank, st_bytes, factors in results:
+        assert np.array_equal(np.frombuffer(st_bytes, np.uint8), want["status"])
+        assert factors == want_factors, rank
+
+
+def test_setup_factor_curves_are_gathered(orc):
+    """Status 4 (the setup gcd is a proper factor) carries a factor too: sigma = 15
+    makes u = 220 = 0 mod 11, so on N = 11 * q the setup gcd is 11."""
+    from workload import ecm_config
+    q = ecm_config(L=6, nbits=190, pbits=32, B1=300, curves=8, seed=1)["q"]
+    N = 11 * q
+    sig = np.array([15, 16, 17, 15, 18], dtype=np.uint64)
+    cfg = {"N": N, "L": 6, "B1": 300, "sigmas": sig}
+    results = _run_world(2, cfg)
+    want, want_factors = _want(orc, cfg)
+    assert want["status"][0] == 4 and want["status"][3] == 4
+    assert (0, 11) in want_factors and (3, 11) in want_factors
+    assert results[0][2] == want_factors
+
+
+def test_compact_factors_fixed_shape():
+    """Device-side compaction: fixed output shape, counts and records in curve order, -1 padding."""
+    from paper_1310_3809_b200.dist import compact_factors, decode_records
+    st = torch.tensor([0, 1, 2, 4, 1, 0, 3, 1], dtype=torch.uint8)
+    g = torch.arange(8 * 2, dtype=torch.int64).view(8, 2)
+    rec = compact_factors(st, g, 100, 3)
+    assert rec.shape == (4, 3)
+    assert rec[0, 0] == 4  # curves 1, 3, 4, 7
+    assert rec[1:, 0].tolist() == [101, 103, 104]
+    assert rec[1, 1:].tolist() == [2, 3]
+    full = compact_factors(st, g, 100, 8)
+    assert (full[5:] == -1).all()
+    dec = decode_records(full.numpy(), 1, 8)
+    assert [i for i, _ in dec] == [101, 103, 104, 107]
+    assert dec[0][1] == 2 + (3 << 32)

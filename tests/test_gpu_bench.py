@@ -22,19 +22,26 @@ def _one_line(out):
     return json.loads(lines[0])
 
 
-def test_bench_single_rank_small():
+@pytest.fixture(scope="module")
+def single_rank_line():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *SMALL, "--cpu-elems", "2048",
                         "--cpu-curves", "8", "--cpu-seconds", "0.5"], capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
-    d = _one_line(r.stdout)
+    return _one_line(r.stdout)
+
+
+def test_bench_single_rank_small(single_rank_line):
+    d = single_rank_line
     assert d["n_gpus"] == 1 and d["value"] > 0 and d["gpu_launches"] == 2
     assert d["parity"]["mulmod_mismatches"] == 0 and d["parity"]["ecm_mismatches"] == 0
     for k in ("roofline", "cpu_baseline", "e2e", "clocks", "ecm"):
         assert k in d
+    for k in ("kernel_ms_per_rank", "gather_ms", "status_digest", "factors_digest", "factors_found"):
+        assert k in d["ecm"]
 
 
 @pytest.mark.parametrize("args", [SMALL, SWEEP], ids=["no-sweep", "sweep"])
-def test_bench_two_ranks_torchrun_gloo(args):
+def test_bench_two_ranks_torchrun_gloo(args, single_rank_line):
     env = dict(os.environ, ECM_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "bench.py"), "--gpus", "2",
@@ -43,7 +50,13 @@ def test_bench_two_ranks_torchrun_gloo(args):
     assert r.returncode == 0, r.stderr[-3000:]
     d = _one_line(r.stdout)
     assert d["n_gpus"] == 2 and d["value"] > 0 and "cpu_baseline" not in d
-    assert d["ecm"]["flagged_factor"] >= 0
+    # the sharded + gathered ECM result equals the one-rank run of the same curves, curve by curve
+    one = single_rank_line["ecm"]
+    assert d["ecm"]["flagged_factor"] == one["flagged_factor"]
+    assert d["ecm"]["status_digest"] == one["status_digest"]
+    assert d["ecm"]["factors_digest"] == one["factors_digest"]
+    assert d["ecm"]["curves_per_rank"] == [1024, 1024]
+    assert d["ecm"]["kernel_ms_per_rank"]["max"] >= d["ecm"]["kernel_ms_per_rank"]["min"] > 0
     if args is SWEEP:
         assert set(d["ecm"]["widths"]) == {"L4", "L6", "L8", "L12", "L16"}
         assert d["ecm"]["small_family"]["curves_per_s"] > 0 and "mul_L16" in d["sweep"]

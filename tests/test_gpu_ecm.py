@@ -126,19 +126,20 @@ def test_host_buffers_and_no_xaff(orc, torch):
 
 
 def test_c3_full_size_sampled(orc, torch):
-    """C3 (B1 = 50000, 2^20 curves, 190-bit N with a planted 64-bit p): 256 strided curves
-    bit-exact vs the oracle; every flagged g divides N."""
+    """C3 (B1 = 50000, 2^20 curves, 190-bit N with a planted 64-bit p; the launch bench.py times):
+    4096 strided curves bit-exact vs the oracle (about 20 s on the box's host cores); every flagged
+    g divides N."""
     cfg = ecm_config("C3")
     N, L = cfg["N"], cfg["L"]
     got = gpu_stage1(torch, N, L, cfg["B1"], cfg["sigmas"], want=("X", "Z", "g"))
-    idx = np.arange(0, cfg["curves"], cfg["curves"] // 256) + 7
+    idx = np.arange(0, cfg["curves"], cfg["curves"] // 4096) + 7
     k, _ = orc.stage1_k(cfg["B1"])
     want = orc.ecm_stage1_mt(N, L, k, cfg["sigmas"][idx])
     sub = {key: v[idx] for key, v in got.items()}
     assert_same(sub, want, keys=("X", "Z", "g", "status"))
     flagged = np.nonzero(got["status"] == 1)[0]
     assert len(flagged) > 1000  # Dickman estimate ~7k (SURVEY §8(d) d1)
-    for i in flagged[:: max(1, len(flagged) // 500)]:
+    for i in flagged:
         g = eg.limbs_to_int(got["g"][i])
         assert 1 < g < N and N % g == 0
 
@@ -250,3 +251,18 @@ def test_results_independent_of_sharding(torch):
                  for r in range(w)]
         for key in ("X", "Z", "g", "status", "xaff"):
             assert np.array_equal(np.concatenate([p[key] for p in parts]), full[key]), (w, key)
+
+
+@pytest.mark.parametrize("kernel", ["lanes1", "lanes4"])
+@pytest.mark.parametrize("L", (4, 6, 8, 12, 16))
+def test_near_max_composite_every_width(orc, torch, L, kernel):
+    """ECM on N = p q just below R/4 = 2^(32L-2) (the largest modulus the two spare bits allow,
+    PAPER.md:189) at every width with both kernels: X, Z, g, status, xaff bit-exact vs the oracle."""
+    from workload import near_max_composite, sigmas
+    N, p, q = near_max_composite(L)
+    assert N.bit_length() == 32 * L - 2
+    sig = sigmas(62 + L, 45)
+    k, _ = orc.stage1_k(400)
+    want = orc.ecm_stage1_mt(N, L, k, sig)
+    got = gpu_stage1(torch, N, L, 400, sig, flags=KERNELS[kernel])
+    assert_same(got, want)

@@ -158,8 +158,9 @@ def test_host_buffers_path(orc, torch):
 
 
 def test_c2_full_size(orc, torch):
-    """C2: 2^24 triples, L = 6, the bench launch configuration; K = 1 and 16 element-wise,
-    K = 256 on a strided sample, out < 2N everywhere; AoS == sliced."""
+    """C2: 2^24 triples, L = 6, the bench launch configuration; K = 1, 16 and 256 (the headline)
+    element by element against the oracle (K = 256: 4.3e9 products, about 30 s on the box's host
+    cores), out < 2N everywhere; AoS == sliced."""
     L, count = 6, 1 << 24
     a, b, n = mulmod_inputs(count, L, seed=2)
     A, B, Nn = (dev(torch, x) for x in (a, b, n))
@@ -170,9 +171,8 @@ def test_c2_full_size(orc, torch):
         assert lt_2n(got, n).all()
     got = eg.ecm_mulmod_batch(A, B, Nn, L=L, iters=256).cpu().numpy()
     assert lt_2n(got, n).all()
-    idx = np.arange(0, count, count // (1 << 14)) + 13
-    want = orc.mulmod_chain_mt(a[idx], b[idx], n[idx], L, 256)
-    assert np.array_equal(got[idx], want)
+    want = orc.mulmod_chain_mt(a, b, n, L, 256)
+    assert np.array_equal(got, want)
     # the same triples in the limb-sliced layout give the same outputs (K = 1: streaming kernel)
     S = [dev(torch, x.T.copy()) for x in (a, b, n)]
     g1 = eg.ecm_mulmod_batch(*S, L=L, iters=1, flags=eg.ECM_LAYOUT_SLICED).cpu().numpy().T
@@ -288,3 +288,28 @@ def test_fault_injection_is_detected(orc, torch):
     want = orc.mulmod_chain_mt(a, b, n, L, 8)
     bad = np.nonzero((got != want).any(axis=1))[0]
     assert list(bad) == [17]
+
+
+LAYOUT_KERNELS = {"aos_stream": eg.ECM_KERNEL_STREAM, "aos_warp": eg.ECM_KERNEL_WARP,
+                  "sliced_stream": eg.ECM_LAYOUT_SLICED | eg.ECM_KERNEL_STREAM,
+                  "sliced_warp": eg.ECM_LAYOUT_SLICED | eg.ECM_KERNEL_WARP}
+
+
+@pytest.mark.parametrize("L", (4, 6, 8, 12, 16))
+@pytest.mark.parametrize("variant", list(VARIANTS))
+def test_width_limit_worst_cases(orc, torch, L, variant):
+    """Moduli at and just below R/4 = 2^(32L-2) (top limb 0x3fffffff: the two spare bits of
+    PAPER.md:189 and nothing more), the smallest full-width N and the tiny N = 3, 5, each with every
+    ordered pair of operands from {0, 1, N-1, N, 2N-2, 2N-1}: the accumulator carry bounds of every
+    REDC form are tightest here.  Every width x mul/sqr x AoS/sliced x
+    streaming/warp-tile kernel x REDC variant, bit-exact against the oracle, raw outputs < 2N."""
+    from workload import edge_mulmod_inputs
+    a, b, n = edge_mulmod_inputs(L)  # 432 elements: one full 256-element tile + a ragged tail
+    for square in (False, True):
+        for iters in (1, 3):
+            want = orc.mulmod_chain_mt(a, b, n, L, iters, square=square)
+            assert lt_2n(want, n).all()
+            for name, kf in LAYOUT_KERNELS.items():
+                flags = VARIANTS[variant] | kf | (eg.ECM_SQUARE if square else 0)
+                got = run_gpu(torch, a, b, n, L, iters, flags)
+                assert np.array_equal(got, want), (name, square, iters)

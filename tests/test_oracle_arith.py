@@ -162,3 +162,24 @@ def test_inputs_in_domain():
     a, b, n = mulmod_inputs(100, 6, seed=3)
     a2, b2, n2 = mulmod_inputs(10, 6, seed=3, start=50)
     assert np.array_equal(a[50:60], a2) and np.array_equal(n[50:60], n2)
+
+
+@pytest.mark.parametrize("L", (4, 6, 8, 12, 16))
+@pytest.mark.parametrize("square", (False, True))
+def test_chain_width_limit_edges(orc, L, square):
+    """The width-limit worst cases the GPU tests use (workload.edge_mulmod_inputs: N at and just
+    below R/4, the smallest full-width N, N = 3, 5; operands 0, 1, N-1, N, 2N-2, 2N-1): the raw
+    single step is the unique REDC value (out R = T + qN, 0 <= q < R, out < 2N) and the K = 3
+    chain's canonical value matches the closed form."""
+    from workload import edge_mulmod_inputs
+    a, b, n = edge_mulmod_inputs(L, reps=1)
+    R = 1 << (32 * L)
+    raw1 = orc.mulmod_chain(a, b, n, L, 1, square=square)
+    can3 = orc.mulmod_chain(a, b, n, L, 3, square=square, canonical=True)
+    for ai, bi, ni, r, c in zip(_ints(a), _ints(b), _ints(n), _ints(raw1), _ints(can3)):
+        T = ai * ai if square else ai * bi
+        q, rem = divmod(r * R - T, ni)
+        assert rem == 0 and 0 <= q < R and r < 2 * ni
+        Ri = pow(R, -1, ni)
+        want = pow(ai, 8, ni) * pow(Ri, 7, ni) % ni if square else ai * pow(bi * Ri % ni, 3, ni) % ni
+        assert c == want

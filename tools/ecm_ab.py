@@ -28,12 +28,18 @@ def build(pairs, L=6):
     B.build()
     os.makedirs(VAR, exist_ok=True)
     objs = sorted(os.path.join(B.BUILD, f) for f in os.listdir(B.BUILD) if f.endswith(".o"))
-    srcs = [f"ecm_l{L}.cu", f"mulmod_l{L}.cu"] if L else sorted(f for f in os.listdir(B.CSRC) if f.endswith(".cu"))
+    # single-width library (small enough to ship several to the GPU box): the dispatchers are rebuilt
+    # with -DECM_ONLY_L and only that width's kernels are linked
+    srcs = [f"ecm_l{L}.cu", f"mulmod_l{L}.cu", "ecm.cu", "mulmod.cu"] if L else \
+        sorted(f for f in os.listdir(B.CSRC) if f.endswith(".cu"))
+    if L:
+        objs = [o for o in objs if os.path.basename(o)[:-2] in srcs + ["abi.cu"]]
     jobs = []
     for name, flags in pairs:
         for src in srcs:
             o = os.path.join(VAR, f"{src}_{name}.o")
-            jobs.append((name, src, o, [B.NVCC, *B.ARCH, *B.CFLAGS, *flags.split(), "-c", os.path.join(B.CSRC, src),
+            only = [f"-DECM_ONLY_L={L}"] if L else []
+            jobs.append((name, src, o, [B.NVCC, *B.ARCH, *B.CFLAGS, *only, *flags.split(), "-c", os.path.join(B.CSRC, src),
                                         "-o", o]))
     with cf.ThreadPoolExecutor(max_workers=len(jobs)) as ex:
         for (name, src, o, cmd), r in zip(jobs, ex.map(lambda j: subprocess.run(j[3], capture_output=True, text=True),

@@ -31,12 +31,13 @@ if a.what == "mulmod":
     for _ in range(a.reps):
         eg.ecm_mulmod_batch(x, y, n, L=a.L, iters=a.iters, flags=fl)
 else:
-    cfg = ecm_config(a.cfg)
+    cfg = ecm_config(a.cfg) if a.L == 6 else ecm_config(L=a.L, nbits=32 * a.L - 2, pbits=64, B1=a.B1,
+                                                            curves=a.curves, seed=40 + a.L)
     sig = cfg["sigmas"][: a.curves].copy()
     if a.flags & eg.ECM_CURVE_SMALL:
         sig = (sig % np.uint64((1 << 30) - 1)) + np.uint64(1)
     s = torch.from_numpy(sig).cuda()
     for _ in range(a.reps):
-        eg.ecm_stage1_batch(cfg["N"], 6, a.B1, s, flags=a.flags, want=("g",))
+        eg.ecm_stage1_batch(cfg["N"], a.L, a.B1, s, flags=a.flags, want=("g",))
 torch.cuda.synchronize()
 print("done")

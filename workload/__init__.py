@@ -15,4 +15,7 @@ from .gen import (  # noqa: F401
     ecm_config,
     ECM_CONFIGS,
     MULMOD_CONFIGS,
+    edge_moduli,
+    edge_mulmod_inputs,
+    near_max_composite,
 )

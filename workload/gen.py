@@ -177,3 +177,46 @@ def ecm_config(name: str | None = None, *, L=None, nbits=None, pbits=None, B1=No
     cfg.update(N=p * q, p=p, q=q, sigmas=sigmas(s, cfg["curves"]))
     cfg["name"] = name
     return cfg
+
+
+# ---------------------------------------------------------------------------------------
+# Width-limit worst cases: moduli at and near R/4 = 2^(32L-2), the largest
+# the two spare bits allow, and operands at the ends of the lazy domain [0, 2N).
+# ---------------------------------------------------------------------------------------
+def edge_moduli(L: int, seed: int = 60) -> list[int]:
+    """Odd moduli with bitlen <= 32L-2 where the carry bounds are tightest: 2^(32L-2)-1 (N just
+    below R/4), 2^(32L-2)-3, top limb 0x3fffffff with seeded random lower limbs, the smallest
+    full-width N = 2^(32L-3)+1, and the tiny moduli 3 and 5."""
+    top = 1 << (32 * L - 2)
+    r = int(splitmix64(seed, L, tag=9)) | (int(splitmix64(seed, L, tag=10)) << 64)
+    low = (r | (r << 128) | (r << 256) | (r << 384)) & ((1 << (32 * (L - 1))) - 1)
+    return [top - 1, top - 3, (0x3FFFFFFF << (32 * (L - 1))) | low | 1, (top >> 1) + 1, 3, 5]
+
+
+def edge_mulmod_inputs(L: int, reps: int = 2, seed: int = 60):
+    """(a, b, n) (count, L) uint32 arrays: every modulus of edge_moduli(L) with every ordered pair
+    of operands from {0, 1, N-1, N, 2N-2, 2N-1} (all < 2N), the whole list repeated `reps` times
+    so that a batch spans full tiles and a ragged tail."""
+    rows = []
+    for N in edge_moduli(L, seed):
+        ops = sorted({0, 1, N - 1, N, 2 * N - 2, 2 * N - 1})
+        rows += [(x, y, N) for x in ops for y in ops]
+    rows = rows * reps
+
+    def limbs(v):
+        return [(v >> (32 * j)) & 0xFFFFFFFF for j in range(L)]
+    a = np.array([limbs(x) for x, _, _ in rows], np.uint32)
+    b = np.array([limbs(y) for _, y, _ in rows], np.uint32)
+    n = np.array([limbs(N) for _, _, N in rows], np.uint32)
+    return a, b, n
+
+
+def near_max_composite(L: int, pbits: int = 32, seed: int = 61) -> tuple[int, int, int]:
+    """(N, p, q): N = p*q with a planted pbits-bit prime p and q the largest prime with
+    p*q < 2^(32L-2), so N sits just below R/4."""
+    p = random_prime(1 << (pbits - 1), 1 << pbits, seed, tag=11)
+    q = ((1 << (32 * L - 2)) - 1) // p
+    q -= 1 - (q & 1)
+    while not is_probable_prime(q):
+        q -= 2
+    return p * q, p, q
