@@ -34,18 +34,23 @@ constexpr int kEcmTPB = 128;
 #ifndef ECM_SWAP_BRANCH
 #define ECM_SWAP_BRANCH 0
 #endif
-//   ECM_SWAP_SEL    : 1 (default) = no state swap; the doubling's input sums are selected
-//                     (ladder_step_sel, 2L instead of 4L selects per step); 0 = conditional swap
+//   ECM_SWAP_SEL    : 1 = no state swap; the doubling's input sums are selected (ladder_step_sel,
+//                     2L instead of 4L selects per step); 0 = conditional swap; -1 = per-width default
 #ifndef ECM_SWAP_SEL
-#define ECM_SWAP_SEL 1
+#define ECM_SWAP_SEL -1
 #endif
 //   ECM_LADDER_SQR  : square form in the ladder (mont_sqr FORM; -1 = per-width default below)
 #ifndef ECM_LADDER_SQR
 #define ECM_LADDER_SQR -1
 #endif
-// L = 6 keeps the merged square in the ladder: with the unmerged form the 80-register ladder spills
-// more (profiles/r02a_ab6.jsonl); every other width takes the unmerged form.
-__host__ __device__ constexpr int ladder_sqr_form(int L) { return ECM_LADDER_SQR >= 0 ? ECM_LADDER_SQR : L == 6 ? 0 : 1; }
+// Per-width ladder forms, each the measured best (tools/ecm_ab.py, profiles/r02b_ab*.jsonl): the
+// swap-free step at L <= 8; the unmerged square at L = 4 and 8 (at L = 6 the 80-register ladder
+// spills more with it); L = 12 and 16 keep the conditional swap and the merged square (their
+// 168 / 254-register ladders schedule worse with the extra live sums: -11 % / -5 %).
+__host__ __device__ constexpr bool ladder_swap_sel(int L) { return ECM_SWAP_SEL >= 0 ? ECM_SWAP_SEL != 0 : L <= 8; }
+__host__ __device__ constexpr int ladder_sqr_form(int L) {
+  return ECM_LADDER_SQR >= 0 ? ECM_LADDER_SQR : (L == 4 || L == 8) ? 1 : 0;
+}
 //   ECM_CONST_SMEM  : 1 = x0 and a24 live in shared memory during the ladder (loaded per use)
 #ifndef ECM_CONST_SMEM
 #define ECM_CONST_SMEM 0
@@ -660,17 +665,13 @@ __global__ void __launch_bounds__(kEcmTPB, ecm_min_blocks(L, VAR, EAGER, PRIMES)
         // bit is warp-uniform, so this is a uniform branch between two copies of the step.
         if (bit) ladder_step<L>(X1, Z1, X0, Z0, x0, a24, fld);
         else ladder_step<L>(X0, Z0, X1, Z1, x0, a24, fld);
-#elif ECM_SWAP_SEL
-        // slot 0 holds R_swapped: double slot (bit != swapped), write the double to slot 0
-        if (FAM == 1) {
-          cswap<L>(X0, X1, bit != swapped);
-          cswap<L>(Z0, Z1, bit != swapped);
-          ladder_step_small<L>(X0, Z0, X1, Z1, cs, N, n0inv, fld);
-        } else {
-          ladder_step_sel<L>(X0, Z0, X1, Z1, x0, a24, fld, bit != swapped);
-        }
-        swapped = bit;
 #else
+        if constexpr (ladder_swap_sel(L) && FAM == 0 && !ECM_CONST_SMEM) {
+          // slot 0 holds R_swapped: double slot (bit != swapped), write the double to slot 0
+          ladder_step_sel<L>(X0, Z0, X1, Z1, x0, a24, fld, bit != swapped);
+          swapped = bit;
+          continue;
+        }
         // bit 1: (R0, R1) <- (xADD, xDBL(R1)); bit 0: (xDBL(R0), xADD).  Double the point in the
         // (X0,Z0) slot: swap so that slot holds R_bit, swap back lazily on the next change.
         cswap<L>(X0, X1, bit != swapped);

@@ -240,7 +240,8 @@ def _random_triples_on_device(torch, count, L, sliced, seed):
     for x in (a, b):
         xt = top(x)
         xt.copy_(torch.remainder(xt, nt))  # top limb < n's -> x < n
-    return a, b, n
+    # the arithmetic above needs int32 ops; the ABI takes uint32 limbs (same bits)
+    return a.view(torch.uint32), b.view(torch.uint32), n.view(torch.uint32)
 
 
 @pytest.mark.parametrize("layout", ("aos", "sliced"))
