@@ -528,7 +528,9 @@ def main():
     ap.add_argument("--iters", type=int, default=C2_ITERS)
     ap.add_argument("--no-ecm", action="store_true")
     ap.add_argument("--ecm-curves", type=int, default=None)
-    ap.add_argument("--ecm-width-curves", type=int, default=1 << 17, help="curves per width in the ECM width sweep")
+    # 148 SMs x 128 threads x 12: whole waves at 6, 3 and 2 resident CTAs per SM (the ladder's occupancy at
+    # L <= 6, 8 / 12 and 16), so no width's number carries a partly filled last wave
+    ap.add_argument("--ecm-width-curves", type=int, default=148 * 128 * 12, help="curves per width in the ECM width sweep")
     ap.add_argument("--ecm-b1", type=int, default=None, help="override C3's B1 (tests / profiling only)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")

@@ -262,7 +262,8 @@ def test_max_size_64bit_offsets(orc, torch, layout):
                                     [(1 << 32) // L - 1, (1 << 32) // L, (1 << 32) // L + 1]]))
     it = torch.from_numpy(idx).cuda()
 
-    def rows(t):  # (len(idx), L) host copies of the sampled elements
+    def rows(t):  # (len(idx), L) host copies of the sampled elements (CUDA indexing needs int32)
+        t = t.view(torch.int32)
         r = t[:, it].t() if sliced else t[it]
         return r.contiguous().cpu().numpy().view(np.uint32)
 
