@@ -64,12 +64,12 @@ def main():
     tot_i = sum(x["inst"] for x in ins) or 1.0
     res = {}
     for name, pred in (("setup", lambda a: a < lo), ("ladder", lambda a: lo <= a <= hi), ("tail", lambda a: a > hi),
-                       ("xgcd_loops", lambda a: any(p <= a <= q for p, q in xg))):
+                       ("xgcd", lambda a: any(p <= a <= q for p, q in xg))):
         s = sum(x["samples"] for x in ins if pred(x["addr"]))
         i = sum(x["inst"] for x in ins if pred(x["addr"]))
         res[name] = {"stall_sample_share": s / tot_s, "inst_share": i / tot_i}
     res["ladder_addr"] = [hex(lo), hex(hi)]
-    res["xgcd_loops"] = [[hex(a), hex(b)] for a, b in xg]
+    res["xgcd_loop_addr"] = [[hex(a), hex(b)] for a, b in xg]
     if "--json" in sys.argv:
         print(json.dumps(res))
     else:
