@@ -157,6 +157,30 @@ def test_host_buffers_path(orc, torch):
     assert np.array_equal(out, orc.mulmod_chain(a, b, n, L, 4))
 
 
+@pytest.mark.parametrize("iters", [1, 8])
+@pytest.mark.parametrize("sliced", [False, True])
+def test_host_buffers_with_check_odd_count(orc, torch, iters, sliced):
+    """ECM_HOST_BUFFERS | ECM_CHECK stages a, b, n and out in one device scratch block; at L = 6 with an
+    odd count the per-array strides must still be 16-byte aligned for the bulk copies and 128-bit
+    accesses of both kernels (count >= 257: the streaming kernel at iters 1, the warp kernel at 8)."""
+    L, count = 6, 32 * 9 + 1
+    a, b, n = mulmod_inputs(count, L, seed=19, lazy=True)
+    ref = orc.mulmod_chain(a, b, n, L, iters)
+    fl = eg.ECM_HOST_BUFFERS | eg.ECM_CHECK
+    if sliced:
+        out = eg.ecm_mulmod_batch(a.T.copy(), b.T.copy(), n.T.copy(), L=L, iters=iters,
+                                  flags=fl | eg.ECM_LAYOUT_SLICED)
+        assert np.array_equal(out.T, ref)
+    else:
+        out = eg.ecm_mulmod_batch(a, b, n, L=L, iters=iters, flags=fl)
+        assert np.array_equal(out, ref)
+    bad = n.copy()
+    bad[count - 1, 0] &= ~np.uint32(1)  # even modulus on the last element
+    with pytest.raises(eg.EcmError) as e:
+        eg.ecm_mulmod_batch(a, b, bad, L=L, iters=iters, flags=fl)
+    assert e.value.status == 2
+
+
 def test_c2_full_size(orc, torch):
     """C2: 2^24 triples, L = 6, the bench launch configuration; K = 1, 16 and 256 (the headline)
     element by element against the oracle (K = 256: 4.3e9 products, about 30 s on the box's host
