@@ -43,14 +43,20 @@ constexpr int kEcmTPB = 128;
 #ifndef ECM_LADDER_SQR
 #define ECM_LADDER_SQR -1
 #endif
-// Per-width ladder forms, each the measured best (tools/ecm_ab.py, profiles/r02b_ab*.jsonl): the
-// swap-free step at L <= 8; the unmerged square at L = 4 and 8 (at L = 6 the 80-register ladder
-// spills more with it); L = 12 and 16 keep the conditional swap and the merged square (their
-// 168 / 254-register ladders schedule worse with the extra live sums: -11 % / -5 %).
+// Per-width ladder forms, each the measured best (tools/ecm_ab.py, profiles/r02b_ab*.jsonl,
+// r02e_ab*.jsonl): the swap-free step at L <= 8 (L = 12 and 16 keep the conditional swap: their
+// 168 / 254-register ladders schedule worse with the extra live sums, -11 % / -5 %); the square on
+// offset chains (mont.cuh FORM 2 / 3) instead of rows: FORM 3 (high half added at the end) at L = 4, 6
+// and 16, FORM 2 (high half injected into the reduction frame) at L = 8 and 12 — against the previous
+// row forms +2.2 / +0.9 / +1.7 / +0.7 / +2.4 % curves/s at L = 4 / 6 / 8 / 12 / 16.
 __host__ __device__ constexpr bool ladder_swap_sel(int L) { return ECM_SWAP_SEL >= 0 ? ECM_SWAP_SEL != 0 : L <= 8; }
 __host__ __device__ constexpr int ladder_sqr_form(int L) {
-  return ECM_LADDER_SQR >= 0 ? ECM_LADDER_SQR : (L == 4 || L == 8) ? 1 : 0;
+  return ECM_LADDER_SQR >= 0 ? ECM_LADDER_SQR : (L == 8 || L == 12) ? 2 : 3;
 }
+//   ECM_MULADD      : 1 = d + a24 t as one REDC frame with d injected (Field::mul_add)
+#ifndef ECM_MULADD
+#define ECM_MULADD 0
+#endif
 //   ECM_CONST_SMEM  : 1 = x0 and a24 live in shared memory during the ladder (loaded per use)
 #ifndef ECM_CONST_SMEM
 #define ECM_CONST_SMEM 0
@@ -257,6 +263,20 @@ struct Field {
   __device__ __forceinline__ void add(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L]) const {
     add_lazy<L>(r, x, y, M);
   }
+  // r = d + x y: with ECM_MULADD the addend enters the product's REDC frame (mont_mul_add, no add
+  // instructions) and only the conditional subtraction of 2N remains
+  __device__ __forceinline__ void mul_add(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L],
+                                          const uint32_t (&d)[L]) const {
+    if constexpr (V == REDC_WORD && !EAGER && ECM_MULADD != 0) {
+      mont_mul_add<L>(r, x, y, d, N, n0inv);
+      reduce_2n<L>(r, M);
+      debug_lazy_bound<L>(r, N);
+    } else {
+      uint32_t t[L];
+      mul(t, x, y);
+      add(r, d, t);
+    }
+  }
   __device__ __forceinline__ void sub(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L]) const {
     sub_lazy<L>(r, x, y, M);
   }
@@ -284,8 +304,7 @@ __device__ __forceinline__ void ladder_step(uint32_t (&X0)[L], uint32_t (&Z0)[L]
   f.sqr(d, t2);
   f.mul(X0, s, d);
   f.sub(t1, s, d);   // t
-  f.mul(t2, a24, t1); // a24 t
-  f.add(t2, d, t2);  // d + a24 t
+  f.mul_add(t2, a24, t1, d);  // d + a24 t
   f.mul(Z0, t1, t2);
   f.add(t3, U, V);
   f.sub(t4, U, V);
@@ -320,8 +339,7 @@ __device__ __forceinline__ void ladder_step_sel(uint32_t (&X0)[L], uint32_t (&Z0
   f.sqr(d, t2);
   f.mul(X0, s, d);
   f.sub(t1, s, d);   // t
-  f.mul(t2, a24, t1); // a24 t
-  f.add(t2, d, t2);  // d + a24 t
+  f.mul_add(t2, a24, t1, d);  // d + a24 t
   f.mul(Z0, t1, t2);
   f.add(t3, U, V);
   f.sub(t4, U, V);

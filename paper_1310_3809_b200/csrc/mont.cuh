@@ -145,6 +145,47 @@ __device__ __forceinline__ void mont_mul_cios(uint32_t (&r)[L], const uint32_t (
   }
 }
 
+// r = REDC(x*y) + d (< 4N for d < 2N) with no addition instructions: REDC(x y + d R) = REDC(x y) + d
+// because q depends only on x y mod R, and word d_i (original weight R 2^(32i)) is placed into the
+// slot that is zero after row i's shift (O[L-2], weight L-1), as in mont_sqr_inj.  Frame bound: the
+// running value stays < y + N + R, and a row adds < 2^32 (y + N): < (3/4) 2^(32(L+1)) for y < 2N.
+template <int L>
+__device__ __forceinline__ void mont_mul_add(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&y)[L],
+                                             const uint32_t (&d)[L], const uint32_t (&n)[L], uint32_t n0inv) {
+  uint32_t E[L], O[L], Z[L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) Z[j] = 0;
+  chain<L, 1, false, false>(O, Z, x[0], y);
+  chain<L, 0, false, false>(E, Z, x[0], y);
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    if (i > 0) {
+      chain<L, 1, true, false>(O, O, x[i], y);
+      chain<L, 0, false, true>(E, E, x[i], y);
+      O[L - 1] = ptx::addc(O[L - 1], 0);
+    }
+    const uint32_t m = E[0] * n0inv;
+    chain<L, 1, false, false>(O, O, m, n);
+    chain<L, 0, false, true>(E, E, m, n);
+    O[L - 1] = ptx::addc(O[L - 1], 0);
+    uint32_t nE[L], nO[L];
+#pragma unroll
+    for (int k = 0; k < L; ++k) nE[k] = O[k];
+    nE[0] = ptx::add_cc(nE[0], E[1]);
+#pragma unroll
+    for (int k = 0; k < L; ++k) nO[k] = (k + 2 < L) ? E[k + 2] : (k == L - 2) ? d[i] : 0u;
+    if (i + 1 < L) {
+#pragma unroll
+      for (int k = 0; k < L; ++k) { E[k] = nE[k]; O[k] = nO[k]; }
+    } else {
+      r[0] = nE[0];
+#pragma unroll
+      for (int k = 1; k < L - 1; ++k) r[k] = ptx::addc_cc(nE[k], nO[k - 1]);
+      r[L - 1] = ptx::addc(nE[L - 1], nO[L - 2]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // Block (SOS) forms of REDC, for the paper's ablation (Table 5).
 // T = x*y (2L words); q = (T mod R) * N' mod R; r = (T + q*N)/R.
@@ -441,9 +482,19 @@ __device__ __forceinline__ void mont_mul_kara(uint32_t (&r)[L], const uint32_t (
 //   the reduction frame directly and their high halves are added at the end (5 fewer additions at
 //   L = 6; measured +2.3 % in square mode at L = 4 and 6, profiles/r02a_ab*.jsonl).  FORM 0: T is
 //   merged first.  Both give the same raw value.
+//   FORM 2: the same products regrouped into offset chains (sqr_triangle) and T's high half fed into
+//   the reduction frame's free top slot one word per row (see mont_sqr_inj).
+template <int L, bool INJ = true>
+__device__ __forceinline__ void mont_sqr_inj(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&n)[L],
+                                             uint32_t n0inv);
+
 template <int L, int FORM = 1>
 __device__ __forceinline__ void mont_sqr(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&n)[L], uint32_t n0inv) {
   static_assert(L % 2 == 0 && L >= 2, "L must be even");
+  if constexpr (FORM == 2 || FORM == 3) {
+    mont_sqr_inj<L, FORM == 2>(r, x, n, n0inv);
+    return;
+  }
   uint32_t Y[L];
   Y[0] = x[0] << 1;
 #pragma unroll
@@ -563,6 +614,104 @@ __device__ __forceinline__ void mont_sqr(uint32_t (&r)[L], const uint32_t (&x)[L
 #pragma unroll
   for (int k = 1; k < L - 1; ++k) r[k] = ptx::addc_cc(q[k], T[L + k]);
   r[L - 1] = ptx::addc(q[L - 1], T[2 * L - 1]);
+}
+
+// ------------------------------------------------------------------------------------------
+// FORM 2 of the lazy square (same unique raw value, same (3L^2+L)/2 partial products).
+//   Triangle by offset chains: the products P(i,j) = x_i b_ij (i <= j; b_ii = x_i, b_i,i+1 =
+//   Y_{i+1} & ~1, b_ij = Y_j beyond) sit at word offset o = i + j.  An IMAD.WIDE carry chain may
+//   change both factors at every link, so chain c of parity p takes, at every offset o = p, p+2, ...
+//   that still has more than c products, the product with i = floor(o/2) - c: consecutive links
+//   are disjoint pairs (o, o+1), (o+2, o+3), and every chain runs over a contiguous range of
+//   offsets (the count per offset is unimodal).  A carry absorb is needed only where a chain
+//   stops below the top — ceil(L/2) - 1 + L/2 absorbs instead of the rows' 2L - 1 (L = 6: 5 vs 11).
+//   Each accumulator's partial sums stay <= its final value <= x^2 < 2^(64L), so the even
+//   accumulator's top link never carries out.
+//   Reduction with the high half injected: T = A + B R with A = EV mod R + OD mod R and
+//   B = EV div R + OD div R (< N, since T < 4N^2 <= R N).  q depends only on A mod R, and
+//   (A + qN)/R + B is computed in the CIOS frame of mont_mul_cios by placing word B_i into the
+//   slot that is zero after row i's shift (O[L-2], weight L-1 = original weight R 2^(32i)): no
+//   addition at all.  Frame bound: before row i+1 the frame holds at most
+//   (A + q_{<=i} N)/2^(32(i+1)) + (B mod 2^(32(i+1))) 2^(32(L-i-1)) < 2R/2^32 + N + R, and the row
+//   adds m N < 2^32 N: < (3/4) 2^(32(L+1)), so the chains' carry bounds of mont_mul_cios hold.
+//   Against FORM 1 this saves the triangle's surplus absorbs and the final B + A merge (L adds
+//   remain, for B = EV_high + OD_high).
+// ------------------------------------------------------------------------------------------
+template <int L, int PAR>
+__device__ __forceinline__ void sqr_triangle(uint32_t (&acc)[2 * L], const uint32_t (&x)[L], const uint32_t (&Y)[L],
+                                             const uint32_t (&Ym)[L]) {
+  // Shortest chains first: when chain c stops at offset e, word e + 2 has so far received only the
+  // carries of the (shorter) chains already run, so its absorb cannot overflow; the longer chains
+  // pass over it later with their own carry links.
+#pragma unroll
+  for (int c = L - 1; c >= 0; --c) {
+    int last = -1;
+#pragma unroll
+    for (int o = PAR; o <= 2 * L - 2; o += 2) {
+      const int i = o / 2 - c, j = o - i;
+      if (i < 0 || j > L - 1) continue;  // offset o has at most c products
+      const uint32_t a = x[i];
+      const uint32_t b = (i == j) ? x[i] : (j == i + 1) ? Ym[j] : Y[j];
+      if (last < 0) acc[o] = ptx::mad_lo_cc(a, b, acc[o]);
+      else acc[o] = ptx::madc_lo_cc(a, b, acc[o]);
+      if (o + 1 == 2 * L - 1) acc[o + 1] = ptx::madc_hi(a, b, acc[o + 1]);
+      else acc[o + 1] = ptx::madc_hi_cc(a, b, acc[o + 1]);
+      last = o;
+    }
+    if (last >= 0 && last + 2 <= 2 * L - 1) acc[last + 2] = ptx::addc(acc[last + 2], 0u);
+  }
+}
+
+template <int L, bool INJ>
+__device__ __forceinline__ void mont_sqr_inj(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&n)[L],
+                                             uint32_t n0inv) {
+  uint32_t Y[L], Ym[L];
+  Y[0] = x[0] << 1;
+#pragma unroll
+  for (int k = 1; k < L; ++k) {
+    Y[k] = __funnelshift_l(x[k - 1], x[k], 1);
+    Ym[k] = Y[k] & 0xfffffffeu;
+  }
+  Ym[0] = Y[0];
+  uint32_t EV[2 * L], OD[2 * L];
+#pragma unroll
+  for (int k = 0; k < 2 * L; ++k) { EV[k] = 0; OD[k] = 0; }
+  sqr_triangle<L, 0>(EV, x, Y, Ym);
+  sqr_triangle<L, 1>(OD, x, Y, Ym);
+  uint32_t B[L];
+  B[0] = ptx::add_cc(EV[L], OD[L]);
+#pragma unroll
+  for (int k = 1; k < L - 1; ++k) B[k] = ptx::addc_cc(EV[L + k], OD[L + k]);
+  B[L - 1] = ptx::addc(EV[2 * L - 1], OD[2 * L - 1]);
+  uint32_t E[L], O[L];
+#pragma unroll
+  for (int k = 0; k < L; ++k) { E[k] = EV[k]; O[k] = (k + 1 < L) ? OD[k + 1] : 0u; }
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    const uint32_t m = E[0] * n0inv;
+    if (i == 0) chain<L, 1, false, false>(O, O, m, n);
+    else chain<L, 1, true, false>(O, O, m, n);
+    chain<L, 0, false, true>(E, E, m, n);
+    O[L - 1] = ptx::addc(O[L - 1], 0u);
+    uint32_t nE[L], nO[L];
+#pragma unroll
+    for (int k = 0; k < L; ++k) nE[k] = O[k];
+    nE[0] = ptx::add_cc(nE[0], E[1]);
+#pragma unroll
+    for (int k = 0; k < L; ++k) nO[k] = (k + 2 < L) ? E[k + 2] : (INJ && k == L - 2) ? B[i] : 0u;
+#pragma unroll
+    for (int k = 0; k < L; ++k) { E[k] = nE[k]; O[k] = nO[k]; }
+  }
+  r[0] = E[0];  // + O 2^32 + the last shift's pending carry (at word 1)
+#pragma unroll
+  for (int k = 1; k < L - 1; ++k) r[k] = ptx::addc_cc(E[k], O[k - 1]);
+  r[L - 1] = ptx::addc(E[L - 1], O[L - 2]);
+  if constexpr (!INJ) {  // FORM 3: B added at the end (no injected words: the frame's top pairs stay zero)
+    r[0] = ptx::add_cc(r[0], B[0]);
+#pragma unroll
+    for (int k = 1; k < L - 1; ++k) r[k] = ptx::addc_cc(r[k], B[k]);
+    r[L - 1] = ptx::addc(r[L - 1], B[L - 1]);
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -700,6 +849,18 @@ __device__ __forceinline__ void sub_lazy(uint32_t (&r)[L], const uint32_t (&x)[L
 #pragma unroll
   for (int k = 1; k < L - 1; ++k) r[k] = ptx::addc_cc(d[k], n2[k] & mask);
   r[L - 1] = ptx::addc(d[L - 1], n2[L - 1] & mask);
+}
+
+// x in [0, 4N) -> [0, 2N): subtract 2N when x >= 2N (the reduction half of add_lazy)
+template <int L>
+__device__ __forceinline__ void reduce_2n(uint32_t (&x)[L], const uint32_t (&n2)[L]) {
+  uint32_t d[L];
+  d[0] = ptx::sub_cc(x[0], n2[0]);
+#pragma unroll
+  for (int k = 1; k < L; ++k) d[k] = ptx::subc_cc(x[k], n2[k]);
+  const uint32_t borrow = ptx::subc(0u, 0u);
+#pragma unroll
+  for (int k = 0; k < L; ++k) x[k] = borrow ? x[k] : d[k];
 }
 
 // r = x - N if x >= N else x  (canonical representative of a lazy value in [0, 2N))

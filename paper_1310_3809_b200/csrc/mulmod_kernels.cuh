@@ -38,6 +38,15 @@ constexpr uint32_t kVec16 = 1u << 30;
 #ifndef MULMOD_UNROLL
 #define MULMOD_UNROLL 0  // 0: per-width default below
 #endif
+// Square form of the chains (mont.cuh: 1 = split rows, 2 = offset-chain triangle + injected high half,
+// 3 = offset-chain triangle + high half added at the end), per width the measured best (tools/ecm_ab.py,
+// profiles/r02e_ab*.jsonl, r02f_ab*.jsonl): FORM 3 at L <= 8, FORM 1 at L = 12, FORM 2 at L = 16.
+#ifndef MULMOD_SQR_FORM
+#define MULMOD_SQR_FORM -1
+#endif
+__host__ __device__ constexpr int mulmod_sqr_form(int L) {
+  return MULMOD_SQR_FORM >= 0 ? MULMOD_SQR_FORM : L <= 8 ? 3 : L == 12 ? 1 : 2;
+}
 #ifndef MULMOD_SLICED_MINB
 #define MULMOD_SLICED_MINB 4
 #endif
@@ -193,7 +202,7 @@ __device__ __forceinline__ void mulmod_chain(uint32_t (&x)[L], const uint32_t (&
   for (uint32_t t = iters; t != 0; --t) {
     uint32_t r[L];
     if (V == REDC_WORD || V == REDC_KNOWNLOW) {
-      if (SQUARE && V == REDC_WORD) mont_sqr<L>(r, x, nn, n0inv);
+      if (SQUARE && V == REDC_WORD) mont_sqr<L, mulmod_sqr_form(L)>(r, x, nn, n0inv);
       else if (SQUARE) mont_mul_cios<L, V>(r, x, x, nn, n0inv);
       else mont_mul_cios<L, V>(r, x, y, nn, n0inv);
     } else if (V == REDC_KARATSUBA) {
