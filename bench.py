@@ -320,7 +320,8 @@ def run_ours(args):
     # ---------------- C3: ECM stage 1 curves/s (strong scaling over ranks) ----------------
     ecm, ecm_last = None, {}
     if not args.no_ecm:
-        cfg = ecm_config("C3")
+        # --ecm-curves above C3's 2^20 draws more seeds of the same recipe (e.g. a sustained run)
+        cfg = ecm_config("C3", curves=args.ecm_curves) if (args.ecm_curves or 0) > (1 << 20) else ecm_config("C3")
         if args.ecm_b1:
             cfg["B1"] = args.ecm_b1
         curves = cfg["curves"] if args.ecm_curves is None else args.ecm_curves
