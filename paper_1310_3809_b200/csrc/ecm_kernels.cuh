@@ -43,15 +43,15 @@ constexpr int kEcmTPB = 128;
 #ifndef ECM_LADDER_SQR
 #define ECM_LADDER_SQR -1
 #endif
-// Per-width ladder forms, each the measured best (tools/ecm_ab.py, profiles/r02b_ab*.jsonl,
-// r02e_ab*.jsonl): the swap-free step at L <= 8 (L = 12 and 16 keep the conditional swap: their
-// 168 / 254-register ladders schedule worse with the extra live sums, -11 % / -5 %); the square on
-// offset chains (mont.cuh FORM 2 / 3) instead of rows: FORM 3 (high half added at the end) at L = 4, 6
-// and 16, FORM 2 (high half injected into the reduction frame) at L = 8 and 12 — against the previous
-// row forms +2.2 / +0.9 / +1.7 / +0.7 / +2.4 % curves/s at L = 4 / 6 / 8 / 12 / 16.
+// Per-width ladder forms, each the measured best (tools/ecm_ab.py, profiles/r02b/e/f/i_ab*.jsonl): the
+// swap-free step at L <= 8 (L = 12 and 16 keep the conditional swap: their 168 / 254-register ladders
+// schedule worse with the extra live sums, -11 % / -5 %); the square on offset chains (mont.cuh FORMs
+// 2..5) instead of rows: FORM 4 at L = 4 and 8, FORM 3 at L = 6 and 16, FORM 5 at L = 12 — against the
+// round-1 row forms about +3.6 / +0.9 / +2.6 / +3.4 / +1.7 % curves/s at L = 4 / 6 / 8 / 12 / 16 (across
+// boxes, +-1 %).
 __host__ __device__ constexpr bool ladder_swap_sel(int L) { return ECM_SWAP_SEL >= 0 ? ECM_SWAP_SEL != 0 : L <= 8; }
 __host__ __device__ constexpr int ladder_sqr_form(int L) {
-  return ECM_LADDER_SQR >= 0 ? ECM_LADDER_SQR : (L == 8 || L == 12) ? 2 : 3;
+  return ECM_LADDER_SQR >= 0 ? ECM_LADDER_SQR : (L == 4 || L == 8) ? 4 : L == 12 ? 5 : 3;
 }
 //   ECM_MULADD      : 1 = d + a24 t as one REDC frame with d injected (Field::mul_add)
 #ifndef ECM_MULADD

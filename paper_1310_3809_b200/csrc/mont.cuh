@@ -484,15 +484,16 @@ __device__ __forceinline__ void mont_mul_kara(uint32_t (&r)[L], const uint32_t (
 //   merged first.  Both give the same raw value.
 //   FORM 2: the same products regrouped into offset chains (sqr_triangle) and T's high half fed into
 //   the reduction frame's free top slot one word per row (see mont_sqr_inj).
-template <int L, bool INJ = true>
+template <int L, bool INJ = true, int ORD = 0>
 __device__ __forceinline__ void mont_sqr_inj(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&n)[L],
                                              uint32_t n0inv);
 
 template <int L, int FORM = 1>
 __device__ __forceinline__ void mont_sqr(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&n)[L], uint32_t n0inv) {
   static_assert(L % 2 == 0 && L >= 2, "L must be even");
-  if constexpr (FORM == 2 || FORM == 3) {
-    mont_sqr_inj<L, FORM == 2>(r, x, n, n0inv);
+  if constexpr (FORM >= 2 && FORM <= 5) {
+    // 2 / 3: chain order 0, high half injected / added at the end; 4 / 5: chain order 1, added / injected
+    mont_sqr_inj<L, FORM == 2 || FORM == 5, (FORM >= 4) ? 1 : 0>(r, x, n, n0inv);
     return;
   }
   uint32_t Y[L];
@@ -637,14 +638,22 @@ __device__ __forceinline__ void mont_sqr(uint32_t (&r)[L], const uint32_t (&x)[L
 //   Against FORM 1 this saves the triangle's surplus absorbs and the final B + A merge (L adds
 //   remain, for B = EV_high + OD_high).
 // ------------------------------------------------------------------------------------------
-template <int L, int PAR>
+//   Chain order ORD 0: shortest chains first — when chain c stops at offset e, word e + 2 has so far
+//   received only the carries of the (shorter) chains already run, so a one-word absorb cannot
+//   overflow; but that word and its pair partner are then fresh registers, and the longer chain that
+//   later passes over the pair needs an explicit zero for the partner (ptxas emits HFMA2 / IMAD.MOV
+//   zeros on the fma pipe — the square's bottleneck).
+//   ORD 1: chain 0 (the diagonal, the longest) first, then the others shortest to longest.  Chain 0
+//   writes every pair fresh (RZ addends, no zero registers), and when a later chain c stops at e, the
+//   pair (e+2, e+3) holds chain 0's one product plus at most a carry-in and the +1s of the shorter
+//   chains' absorbs (chains 1..c-1 run after c): <= 2^64 - 2^33 + 2 + L, so the carry is absorbed as
+//   a 64-bit add into the pair (two ALU instructions) and can never carry out of it.
+template <int L, int PAR, int ORD = 0>
 __device__ __forceinline__ void sqr_triangle(uint32_t (&acc)[2 * L], const uint32_t (&x)[L], const uint32_t (&Y)[L],
                                              const uint32_t (&Ym)[L]) {
-  // Shortest chains first: when chain c stops at offset e, word e + 2 has so far received only the
-  // carries of the (shorter) chains already run, so its absorb cannot overflow; the longer chains
-  // pass over it later with their own carry links.
 #pragma unroll
-  for (int c = L - 1; c >= 0; --c) {
+  for (int k = 0; k < L; ++k) {
+    const int c = (ORD == 0) ? L - 1 - k : (k == 0) ? 0 : L - k;
     int last = -1;
 #pragma unroll
     for (int o = PAR; o <= 2 * L - 2; o += 2) {
@@ -658,11 +667,17 @@ __device__ __forceinline__ void sqr_triangle(uint32_t (&acc)[2 * L], const uint3
       else acc[o + 1] = ptx::madc_hi_cc(a, b, acc[o + 1]);
       last = o;
     }
-    if (last >= 0 && last + 2 <= 2 * L - 1) acc[last + 2] = ptx::addc(acc[last + 2], 0u);
+    if (last < 0 || last + 2 > 2 * L - 1) continue;
+    if (ORD == 1 && c > 0 && last + 3 <= 2 * L - 1) {
+      acc[last + 2] = ptx::addc_cc(acc[last + 2], 0u);
+      acc[last + 3] = ptx::addc(acc[last + 3], 0u);
+    } else {
+      acc[last + 2] = ptx::addc(acc[last + 2], 0u);
+    }
   }
 }
 
-template <int L, bool INJ>
+template <int L, bool INJ, int ORD>
 __device__ __forceinline__ void mont_sqr_inj(uint32_t (&r)[L], const uint32_t (&x)[L], const uint32_t (&n)[L],
                                              uint32_t n0inv) {
   uint32_t Y[L], Ym[L];
@@ -676,8 +691,8 @@ __device__ __forceinline__ void mont_sqr_inj(uint32_t (&r)[L], const uint32_t (&
   uint32_t EV[2 * L], OD[2 * L];
 #pragma unroll
   for (int k = 0; k < 2 * L; ++k) { EV[k] = 0; OD[k] = 0; }
-  sqr_triangle<L, 0>(EV, x, Y, Ym);
-  sqr_triangle<L, 1>(OD, x, Y, Ym);
+  sqr_triangle<L, 0, ORD>(EV, x, Y, Ym);
+  sqr_triangle<L, 1, ORD>(OD, x, Y, Ym);
   uint32_t B[L];
   B[0] = ptx::add_cc(EV[L], OD[L]);
 #pragma unroll

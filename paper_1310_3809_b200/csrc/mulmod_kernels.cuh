@@ -38,14 +38,15 @@ constexpr uint32_t kVec16 = 1u << 30;
 #ifndef MULMOD_UNROLL
 #define MULMOD_UNROLL 0  // 0: per-width default below
 #endif
-// Square form of the chains (mont.cuh: 1 = split rows, 2 = offset-chain triangle + injected high half,
-// 3 = offset-chain triangle + high half added at the end), per width the measured best (tools/ecm_ab.py,
-// profiles/r02e_ab*.jsonl, r02f_ab*.jsonl): FORM 3 at L <= 8, FORM 1 at L = 12, FORM 2 at L = 16.
+// Square form of the chains (mont.cuh mont_sqr: 1 = split rows; 2..5 = offset-chain triangle with chain
+// order 0 (2, 3) or 1 (4, 5), the high half injected into the reduction frame (2, 5) or added at the end
+// (3, 4)), per width the measured best (tools/ecm_ab.py; profiles/r02e/f/i_ab*.jsonl): FORM 4 at L <= 8
+// (square mode L = 4 / 6: 0.746 / 0.824 with FORM 1 -> 0.796 / 0.857), FORM 1 at L = 12, FORM 2 at L = 16.
 #ifndef MULMOD_SQR_FORM
 #define MULMOD_SQR_FORM -1
 #endif
 __host__ __device__ constexpr int mulmod_sqr_form(int L) {
-  return MULMOD_SQR_FORM >= 0 ? MULMOD_SQR_FORM : L <= 8 ? 3 : L == 12 ? 1 : 2;
+  return MULMOD_SQR_FORM >= 0 ? MULMOD_SQR_FORM : L <= 8 ? 4 : L == 12 ? 1 : 2;
 }
 #ifndef MULMOD_SLICED_MINB
 #define MULMOD_SLICED_MINB 4
