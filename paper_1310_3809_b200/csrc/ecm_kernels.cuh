@@ -360,10 +360,11 @@ __device__ __forceinline__ void lds_res(uint32_t (&d)[L], const uint32_t* base) 
 #pragma unroll
   for (int k = 0; k < L; ++k) d[k] = lds_u32(base + k * TPB);
 }
-template <int L, int TPB, class F>
+// SEL: the swap-free form of ladder_step_sel (`csel` picks the doubling's input sums).
+template <int L, int TPB, bool SEL = false, class F>
 __device__ __forceinline__ void ladder_step_sm(uint32_t (&X0)[L], uint32_t (&Z0)[L], uint32_t (&X1)[L],
                                                uint32_t (&Z1)[L], const uint32_t* sx0, const uint32_t* sa24,
-                                               const F& f) {
+                                               const F& f, bool csel = false) {
   uint32_t t1[L], t2[L], t3[L], t4[L], U[L], V[L], s[L], d[L], c[L];
   f.add(t1, X0, Z0);
   f.sub(t2, X0, Z0);
@@ -371,6 +372,13 @@ __device__ __forceinline__ void ladder_step_sm(uint32_t (&X0)[L], uint32_t (&Z0)
   f.sub(t4, X1, Z1);
   f.mul(U, t2, t3);
   f.mul(V, t1, t4);
+  if constexpr (SEL) {
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+      t1[k] = csel ? t3[k] : t1[k];
+      t2[k] = csel ? t4[k] : t2[k];
+    }
+  }
   f.sqr(s, t1);
   f.sqr(d, t2);
   f.mul(X0, s, d);
@@ -684,9 +692,14 @@ __global__ void __launch_bounds__(kEcmTPB, ecm_min_blocks(L, VAR, EAGER, PRIMES)
         if (bit) ladder_step<L>(X1, Z1, X0, Z0, x0, a24, fld);
         else ladder_step<L>(X0, Z0, X1, Z1, x0, a24, fld);
 #else
-        if constexpr (ladder_swap_sel(L) && FAM == 0 && !ECM_CONST_SMEM) {
+        if constexpr (ladder_swap_sel(L) && FAM == 0) {
           // slot 0 holds R_swapped: double slot (bit != swapped), write the double to slot 0
+#if ECM_CONST_SMEM
+          ladder_step_sm<L, kEcmTPB, true>(X0, Z0, X1, Z1, &sm_c[0][0][threadIdx.x], &sm_c[1][0][threadIdx.x], fld,
+                                           bit != swapped);
+#else
           ladder_step_sel<L>(X0, Z0, X1, Z1, x0, a24, fld, bit != swapped);
+#endif
           swapped = bit;
           continue;
         }
