@@ -237,8 +237,28 @@ ecm_status run_ecm(const uint32_t* N_host, int L, const uint32_t* kw_dev, uint32
 // through three internal streams, so the host->device copy of chunk c+1, the kernel of chunk c and
 // the device->host copy of chunk c-1 overlap (copy engines and SMs run concurrently).  Chunks are
 // whole waves of the kernel that runs them (SMs x resident CTAs x elements per CTA), so no chunk
-// ends in a partly filled wave; the first chunk is one wave, so the pipeline fills in one small
-// copy, and the rest are about count/32 elements each.
+// ends in a partly filled wave.  Chunk sizes ramp up from one wave by about 1.5x per chunk to the
+// cap (about count/32): a chunk's host->device copy must fit in the previous chunk's kernel time, or
+// the SMs idle (at L = 6, K = 256 a wave copies in ~0.2 ms and computes in ~0.33 ms); the last chunks
+// are one wave and the ragged rest, so the final device->host copy is short.
+std::vector<size_t> pipeline_chunks(size_t count, size_t wave) {
+  const size_t nw = count / wave, ragged = count % wave;
+  size_t capw = (count / 32 + wave - 1) / wave;  // cap in waves
+  if (capw < 1) capw = 1;
+  std::vector<size_t> sizes;
+  size_t rem = nw, gw = 1;  // waves per chunk: 1, 1, 2, 3, 4, 6, 9, ... up to the cap; the last one is 1
+  while (rem > 1) {
+    size_t t = gw < capw ? gw : capw;
+    if (t > rem - 1) t = rem - 1;
+    sizes.push_back(t * wave);
+    rem -= t;
+    if (sizes.size() >= 2) gw = (gw * 3 / 2 > gw + 1) ? gw * 3 / 2 : gw + 1;
+  }
+  if (rem) sizes.push_back(rem * wave);  // the last whole wave
+  if (ragged) sizes.push_back(ragged);   // the ragged rest on its own: a limb-sliced chunk whose count is
+                                         // not a multiple of 4 takes the slower unaligned path
+  return sizes;
+}
 constexpr int kPipeStreams = 3;
 cudaError_t mulmod_host_pipelined(const uint32_t* a, const uint32_t* b, const uint32_t* n, uint32_t* out,
                                   size_t count, int L, uint32_t iters, uint32_t flags, cudaStream_t s) {
@@ -248,9 +268,12 @@ cudaError_t mulmod_host_pipelined(const uint32_t* a, const uint32_t* b, const ui
   cudaError_t e = ecm::launch_mulmod(nullptr, nullptr, nullptr, nullptr, (size_t)1 << 24, L, iters, flags, s, &wave);
   if (e != cudaSuccess) return e;
   if (wave == 0) wave = 1u << 16;
-  size_t chunk = (count / 32 + wave - 1) / wave * wave;
-  if (chunk < wave) chunk = wave;
-  const size_t cw = chunk * (size_t)L;  // words per array per slot
+  const std::vector<size_t> plan = pipeline_chunks(count, wave);
+  size_t chunk = 0;
+  for (size_t m : plan) chunk = m > chunk ? m : chunk;
+  // words per array per slot, rounded up to 128 bytes: the last chunk carries the ragged rest (any
+  // count), and every sub-array must stay 16-byte aligned for the bulk copies and 128-bit accesses
+  const size_t cw = (chunk * (size_t)L + 31) & ~(size_t)31;
   uint32_t* scratch = nullptr;
   e = dev_alloc(&scratch, kPipeStreams * 4 * cw * sizeof(uint32_t), s);
   if (e != cudaSuccess) return e;
@@ -261,9 +284,8 @@ cudaError_t mulmod_host_pipelined(const uint32_t* a, const uint32_t* b, const ui
   for (int i = 0; i < kPipeStreams && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventRecord(start, s);
   for (int i = 0; i < kPipeStreams && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(st[i], start, 0);
-  for (size_t c0 = 0, c = 0; c0 < count && e == cudaSuccess; ++c) {
-    const size_t want = c == 0 ? wave : chunk;
-    const size_t m = (count - c0) < want ? (count - c0) : want;
+  for (size_t c0 = 0, c = 0; c < plan.size() && e == cudaSuccess; ++c) {
+    const size_t m = plan[c];
     const size_t by = m * (size_t)L * sizeof(uint32_t);
     cudaStream_t q = st[c % kPipeStreams];
     uint32_t* base = scratch + (c % kPipeStreams) * 4 * cw;

@@ -233,6 +233,24 @@ def test_host_buffers_pipelined_sliced(orc, torch):
         assert np.array_equal(out.numpy().T, want), iters
 
 
+@pytest.mark.parametrize("sliced", [False, True])
+def test_host_buffers_chunk_ramp(orc, torch, sliced):
+    """A batch of ~20 waves through ECM_HOST_BUFFERS runs the whole chunk plan (abi.cu
+    pipeline_chunks: 1, 1, 2, 3, 4, ... waves up to the cap, the last wave with the ragged rest) on
+    both mulmod kernels (iters 1: streaming, 8: warp tiles); every element equals the oracle."""
+    L, count = 6, 3_000_017
+    a, b, n = mulmod_inputs(count, L, seed=21, lazy=True)
+    for iters in (1, 8):
+        if sliced:
+            sa, sb, sn = (torch.from_numpy(x.T.copy()).pin_memory() for x in (a, b, n))
+            out = torch.empty_like(sa).pin_memory()
+            eg.ecm_mulmod_batch(sa, sb, sn, out, L=L, iters=iters, flags=eg.ECM_HOST_BUFFERS | eg.ECM_LAYOUT_SLICED)
+            got = out.numpy().T
+        else:
+            got = eg.ecm_mulmod_batch(a, b, n, L=L, iters=iters, flags=eg.ECM_HOST_BUFFERS)
+        assert np.array_equal(got, orc.mulmod_chain_mt(a, b, n, L, iters)), iters
+
+
 def test_stream_kernel_in_place(orc, torch):
     """out may alias a (include/ecmgpu.h): the streaming kernel's prefetch never reads a tile
     after its output was stored."""
