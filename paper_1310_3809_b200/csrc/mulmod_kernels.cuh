@@ -191,16 +191,43 @@ __device__ __forceinline__ void store_aos(uint32_t* __restrict__ g, const uint32
 // then the optional canonicalisation.  Unrolled by 4: ptxas then keeps the carry absorbs on the
 // ALU pipe and renames instead of copying (SASS: 2 IMAD.X per 4 products instead of 5-7 per
 // product; tools/loopcount.py).
-template <int L, int V, bool SQUARE>
+// n0' = -N^{-1} mod 2^32 parked in a per-thread shared-memory slot and re-read once per product (an
+// LDS on the MIO pipe): under the register cap ptxas otherwise rematerialises the Newton iteration
+// (5 IMAD on the fma pipe, the chains' bottleneck) at the top of every unrolled block.  Limb-sliced
+// warp-tile kernels only, per width the measured best (profiles/r02o_ab.jsonl, r02p_ab.jsonl: same
+// process and box, alternating rounds, fractions of the IMAD.WIDE peak): L = 6 multiply 0.907 -> 0.911,
+// square 0.856 -> 0.861; L = 4 square 0.795 -> 0.797; L = 12 square 0.898 -> 0.900; L = 16 multiply
+// 0.932 -> 0.934, square 0.874 -> 0.879.  Kept in a register: L = 4 multiply (-0.5 %), L = 8 square
+// (-0.7 %), L = 8 / 12 multiply (no change) and the AoS kernels (L = 6: -0.2 % / -1 %).
+// MULMOD_N0_SMEM=0/1 forces it.
+#ifndef MULMOD_N0_SMEM
+#define MULMOD_N0_SMEM -1
+#endif
+__host__ __device__ constexpr bool mulmod_n0_smem(int L, int V, bool square) {
+  return MULMOD_N0_SMEM >= 0 ? MULMOD_N0_SMEM != 0
+                             : V == REDC_WORD && (L == 6 || L == 16 || (square && (L == 4 || L == 12)));
+}
+__device__ __forceinline__ uint32_t ld_volatile_shared(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+  return v;
+}
+// N0SLOT: the caller is the limb-sliced warp-tile kernel (the streaming kernel, K <= 4, keeps n0' in a
+// register and its shared memory for the copy ring).
+template <int L, int V, bool SQUARE, bool N0SLOT = false>
 __device__ __forceinline__ void mulmod_chain(uint32_t (&x)[L], const uint32_t (&y)[L], const uint32_t (&nn)[L],
                                              uint32_t iters, bool canon) {
-  const uint32_t n0inv = neg_inv32(nn[0]);
+  constexpr bool kN0Smem = N0SLOT && mulmod_n0_smem(L, V, SQUARE);
+  __shared__ uint32_t s_n0inv[kN0Smem ? kMulmodTPB : 1];
+  const uint32_t n0reg = neg_inv32(nn[0]);
+  if (kN0Smem) s_n0inv[threadIdx.x] = n0reg;
   uint32_t np[L], dN[L / 2], sn = 0;
   if (V == REDC_BLOCKTHM || V == REDC_CLASSIC || V == REDC_KARATSUBA) nprime_full<L>(np, nn);
   if (V == REDC_KARATSUBA) kara_consts<L>(dN, sn, nn);
   constexpr int kUnroll = mulmod_unroll(L, V, SQUARE);
 #pragma unroll kUnroll
   for (uint32_t t = iters; t != 0; --t) {
+    const uint32_t n0inv = kN0Smem ? ld_volatile_shared(&s_n0inv[threadIdx.x]) : n0reg;
     uint32_t r[L];
     if (V == REDC_WORD || V == REDC_KNOWNLOW) {
       if (SQUARE && V == REDC_WORD) mont_sqr<L, mulmod_sqr_form(L)>(r, x, nn, n0inv);
@@ -291,7 +318,7 @@ __global__ void __launch_bounds__(kMulmodTPB, mulmod_min_blocks(L, V, SLICED)) m
       load_aos<L>(nn, n, tA, e0, nvalid, lane);
     }
     if (lane >= nvalid) nn[0] |= 1u;  // keep dead lanes' arithmetic well-defined
-    mulmod_chain<L, V, SQUARE>(x, y, nn, iters, canon);
+    mulmod_chain<L, V, SQUARE, SLICED>(x, y, nn, iters, canon);
     if (bulk) {
       // stage-out: each lane writes its own words of tile A (the ones it read), then one lane
       // issues the bulk store; generic-proxy writes are fenced for the async proxy first.

@@ -75,12 +75,14 @@ def decode_records(recs, world: int, cap: int) -> list[tuple[int, int]]:
 def ecm_stage1_distributed(N: int, L: int, B1: int, sigmas, *, group=None, compute=None, device=None,
                            capacity: int | None = None, decode: str = "rank0", events: dict | None = None,
                            local: dict | None = None):
-    """Run this rank's shard of `sigmas` (the FULL per-job seed array, host numpy) and gather.
+    """Run this rank's shard of `sigmas` (the FULL per-job seed array: host numpy, or a uint64 torch
+    tensor — a CUDA tensor stays on the device, so a caller can stage the seeds before timing) and gather.
 
     Returns (status, factors): status is a uint8 tensor of all `count` curves in curve order
     (identical on every rank, on the gather device); factors is the sorted list of (curve_index,
     g) for the curves with status 1 or 4 on rank 0 (and on every rank with decode="all"), None on
-    the other ranks.
+    the other ranks.  decode="defer": no host decode; factors is None and `local` receives the raw
+    gathered records ("recs", "world", "cap") for decode_records() outside a timed region.
     `compute(N, L, B1, sigma_tensor) -> {"status": u8[count_local], "g": u32[count_local, L]}`.
     `events`: optional dict; CUDA events "start", "computed", "gathered" are recorded into it on
     the current stream (kernel time = start..computed, gather time = computed..gathered).
@@ -91,8 +93,10 @@ def ecm_stage1_distributed(N: int, L: int, B1: int, sigmas, *, group=None, compu
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    sig = np.asarray(sigmas, dtype=np.uint64)
-    count = sig.size
+    sig = sigmas if torch.is_tensor(sigmas) else np.asarray(sigmas, dtype=np.uint64)
+    if torch.is_tensor(sig) and sig.dtype != torch.uint64:
+        raise ValueError("sigmas tensor must be uint64")
+    count = int(sig.numel()) if torch.is_tensor(sig) else sig.size
     lo, hi = shard_bounds(count, rank, world)
     # the shard is computed on this rank's GPU (or wherever `compute` wants it); the gather runs
     # on `device` (the NCCL device by default, CPU tensors under gloo)
@@ -108,7 +112,7 @@ def ecm_stage1_distributed(N: int, L: int, B1: int, sigmas, *, group=None, compu
             ev.record()
             events[name] = ev
 
-    shard_sig = torch.from_numpy(sig[lo:hi].copy()).to(compute_dev)
+    shard_sig = (sig[lo:hi] if torch.is_tensor(sig) else torch.from_numpy(sig[lo:hi].copy())).to(compute_dev)
     mark("start")
     res = (compute or _default_compute)(N, L, B1, shard_sig)
     mark("computed")
@@ -148,6 +152,10 @@ def ecm_stage1_distributed(N: int, L: int, B1: int, sigmas, *, group=None, compu
             rec = compact_factors(st, g, lo, cap)
             recs = torch.empty((world * (cap + 1), 1 + L), dtype=torch.int64, device=device)
             dist.all_gather_into_tensor(recs, rec, group=group)
+    if decode == "defer":
+        if local is not None:
+            local.update(recs=recs, world=world, cap=cap)
+        return status, None
     if decode == "all" or (decode == "rank0" and rank == 0):
         return status, decode_records(recs.cpu().numpy(), world, cap)
     return status, None

@@ -29,13 +29,19 @@ def _oracle_compute(N, L, B1, sig_t):
     return {"status": torch.from_numpy(r["status"]), "g": torch.from_numpy(r["g"].astype(np.int64))}
 
 
-def _worker(rank, world, port, cfg, out_q, capacity=None, decode="rank0"):
+def _worker(rank, world, port, cfg, out_q, capacity=None, decode="rank0", sig_tensor=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        status, factors = ecm_stage1_distributed(cfg["N"], cfg["L"], cfg["B1"], cfg["sigmas"],
+        sig = torch.from_numpy(cfg["sigmas"].copy()) if sig_tensor else cfg["sigmas"]
+        loc = {}
+        status, factors = ecm_stage1_distributed(cfg["N"], cfg["L"], cfg["B1"], sig,
                                                  compute=_oracle_compute, device="cpu", capacity=capacity,
-                                                 decode=decode)
+                                                 decode=decode, local=loc)
+        if decode == "defer":  # the bench's timed step: records decoded afterwards, outside the call
+            from paper_1310_3809_b200.dist import decode_records
+            assert factors is None
+            factors = decode_records(loc["recs"].numpy(), loc["world"], loc["cap"]) if rank == 0 else None
         out_q.put((rank, status.numpy().tobytes(), factors))
     finally:
         dist.destroy_process_group()
@@ -83,6 +89,21 @@ def test_gloo_gather_equals_single_process(orc, world):
         # rank 0 decodes the gathered records; the other ranks only hold the tensors
         assert factors == (want_factors if rank == 0 else None), rank
     assert len(want_factors) > 0
+
+
+def test_gloo_tensor_seeds_deferred_decode(orc):
+    """bench.py's form of the call: the seeds as a (device-staged) uint64 tensor and decode="defer" —
+    the same statuses and, decoded from the raw records afterwards, the same factor list."""
+    from workload import ecm_config
+    cfg = ecm_config(L=6, nbits=190, pbits=32, B1=300, curves=75, seed=1)
+    cfg = {k: cfg[k] for k in ("N", "L", "B1", "sigmas")}
+    results = _run_world(2, cfg, decode="defer", sig_tensor=True)
+    want, want_factors = _want(orc, cfg)
+    for rank, st_bytes, factors in results:
+        assert np.array_equal(np.frombuffer(st_bytes, np.uint8), want["status"]), rank
+        assert factors == (want_factors if rank == 0 else None), rank
+    with pytest.raises(ValueError):
+        ecm_stage1_distributed(cfg["N"], 6, 300, torch.zeros(4, dtype=torch.int64), compute=_oracle_compute)
 
 
 def test_gloo_capacity_overflow_regathers(orc):

@@ -72,16 +72,20 @@ def time_one(name, curves_list, B1, L):
         from workload import mulmod_inputs
         a, b, n = (torch.from_numpy(v.T.copy()).cuda() for v in mulmod_inputs(1 << 24, L, seed=2))
         out = torch.empty_like(a)
-        for tag, fl in (("mul", eg.ECM_LAYOUT_SLICED), ("sqr", eg.ECM_LAYOUT_SLICED | eg.ECM_SQUARE)):
+        tags = [("mul", eg.ECM_LAYOUT_SLICED), ("sqr", eg.ECM_LAYOUT_SLICED | eg.ECM_SQUARE)]
+        if os.environ.get("AB_AOS") == "1":  # the AoS kernels on the same arrays read as AoS triples
+            tags += [("aos_mul", 0), ("aos_sqr", eg.ECM_SQUARE)]
+        for tag, fl in tags:
             eg.ecm_mulmod_batch(a, b, n, out, L=L, iters=256, flags=fl)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            for _ in range(3):
+            reps = int(os.environ.get("AB_REPS", "3"))
+            for _ in range(reps):
                 eg.ecm_mulmod_batch(a, b, n, out, L=L, iters=256, flags=fl)
             e1.record()
             torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / 3
-            fpe = 2 * L * L if tag == "mul" else (3 * L * L + L) // 2
+            ms = e0.elapsed_time(e1) / reps
+            fpe = 2 * L * L if tag.endswith("mul") else (3 * L * L + L) // 2
             print(json.dumps({"variant": name, "mulmod": tag, "L": L, "ms": ms, "modmul_per_s": (1 << 24) * 256 / ms * 1e3,
                               "frac": (1 << 24) * 256 * fpe / (ms * 1e-3) / (148 * 32 * 1965e6),
                               "out_sum": int(out[:, :4096].to(torch.int64).sum().item())}), flush=True)
