@@ -32,8 +32,10 @@ constexpr uint32_t kVec16 = 1u << 30;
 // Chain-loop unroll and the limb-sliced L <= 6 kernels' occupancy (tools/ecm_ab.py variants,
 // DESIGN.md §6.2): unrolled by 8 and held to 64 registers (4 CTAs x 8 warps per SM), the L = 6
 // sliced chains measured +0.6 % (multiply) and +3.5 % (square) over unroll 4 / 76 registers.
-// Per width (multiply / square, word REDC): L = 4: 8 / 16, L = 6: 8 / 8, L = 8: 2 / 8,
-// L = 12, 16: 2 / 2 — each the best of {2, 4, 8, 16} measured; other REDC variants keep 4.
+// Per width (multiply / square, word REDC): L = 4: 8 / 16, L = 6: 8 / 16, L = 8: 2 / 8,
+// L = 12, 16: 2 / 2 — each the best of {2, 4, 8, 16} measured; other REDC variants keep 4.  (L = 6 square:
+// 8 until the n0' slot; with it, 16 measured 0.862 -> 0.869 — 8 HFMA2 zeros per 8 squares left on the fma
+// pipe instead of 12 IMAD.X + 4 IMAD.MOV + 6 HFMA2; profiles/r02s_ab.jsonl.)
 // MULMOD_UNROLL / MULMOD_SLICED_MINB override them for experiments.
 #ifndef MULMOD_UNROLL
 #define MULMOD_UNROLL 0  // 0: per-width default below
@@ -54,8 +56,7 @@ __host__ __device__ constexpr int mulmod_sqr_form(int L) {
 __host__ __device__ constexpr int mulmod_unroll(int L, int V, bool square) {
   return MULMOD_UNROLL > 0 ? MULMOD_UNROLL
          : V != 0        ? 4
-         : L <= 4        ? (square ? 16 : 8)
-         : L <= 6        ? 8
+         : L <= 6        ? (square ? 16 : 8)
          : L <= 8        ? (square ? 8 : 2)
                          : 2;
 }
