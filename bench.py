@@ -394,7 +394,7 @@ def run_ours(args):
                                "frac": cps / ws * (kb - 1) * fpe_small / pk["fpe_peak"]}
         del sd
 
-    # ---------------- ECM width sweep (C4's widths for stage 1): 2^17 curves per width ----------------
+    # ---------------- ECM width sweep (C4's widths for stage 1): whole waves per width ----------------
     if ecm is not None and not args.no_sweep:
         ecm["widths"] = {}
         for Lw in (4, 6, 8, 12, 16):
@@ -403,13 +403,18 @@ def run_ours(args):
             sw = torch.from_numpy(cw["sigmas"][rank::ws].copy()).cuda()
             eg.ecm_stage1_batch(cw["N"], Lw, cw["B1"], sw[:1024], want=("g",))
             rw = {}
-            msw, _ = time_steps(torch, lambda: rw.update(eg.ecm_stage1_batch(cw["N"], Lw, cw["B1"], sw, want=("g",))),
-                                1, ws)
-            msw = max_over_ranks(torch, msw, ws)
+            # one launch per timed run, `--ecm-width-reps` runs: the fastest is reported, every run listed
+            # (a single one-launch shot once read 0.85 instead of 0.90 at L = 12, profiles/r02q_bench.jsonl)
+            runs = []
+            for _ in range(args.ecm_width_reps):
+                msr, _ = time_steps(torch, lambda: rw.update(eg.ecm_stage1_batch(cw["N"], Lw, cw["B1"], sw,
+                                                                                want=("g",))), 1, ws)
+                runs.append(max_over_ranks(torch, msr, ws))
+            msw = min(runs)
             cps = args.ecm_width_curves / (msw * 1e-3)
             fpe_w = (kb - 1) * (18 * Lw * Lw + 2 * Lw)
             ecm["widths"][f"L{Lw}"] = {"bits": 32 * Lw - 2, "curves": args.ecm_width_curves, "ms": msw,
-                                       "curves_per_s": cps, "modmul_per_s": cps * (kb - 1) * MULMODS_PER_STEP,
+                                       "ms_runs": runs, "curves_per_s": cps, "modmul_per_s": cps * (kb - 1) * MULMODS_PER_STEP,
                                        "frac": cps / ws * fpe_w / pk["fpe_peak"]}
             del sw
 
@@ -537,6 +542,7 @@ def main():
     # 148 SMs x 128 threads x 12: whole waves at 6, 3 and 2 resident CTAs per SM (the ladder's occupancy at
     # L <= 6, 8 / 12 and 16), so no width's number carries a partly filled last wave
     ap.add_argument("--ecm-width-curves", type=int, default=148 * 128 * 12, help="curves per width in the ECM width sweep")
+    ap.add_argument("--ecm-width-reps", type=int, default=2, help="timed one-launch runs per width (fastest reported)")
     ap.add_argument("--ecm-b1", type=int, default=None, help="override C3's B1 (tests / profiling only)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
