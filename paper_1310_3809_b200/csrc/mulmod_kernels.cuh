@@ -189,9 +189,9 @@ __device__ __forceinline__ void store_aos(uint32_t* __restrict__ g, const uint32
 }
 
 // The hot loop of one lane: x <- REDC(x*y) (or REDC(x^2)) `iters` times, all in registers,
-// then the optional canonicalisation.  Unrolled by 4: ptxas then keeps the carry absorbs on the
-// ALU pipe and renames instead of copying (SASS: 2 IMAD.X per 4 products instead of 5-7 per
-// product; tools/loopcount.py).
+// then the optional canonicalisation.  Unrolled per width (mulmod_unroll): ptxas then keeps the carry
+// absorbs on the ALU pipe and renames instead of copying (SASS: at most 2 IMAD.X per 4 products instead
+// of 5-7 per product; tools/loopcount.py, tests/test_sass.py).
 // n0' = -N^{-1} mod 2^32 parked in a per-thread shared-memory slot and re-read once per product (an
 // LDS on the MIO pipe): under the register cap ptxas otherwise rematerialises the Newton iteration
 // (5 IMAD on the fma pipe, the chains' bottleneck) at the top of every unrolled block.  Limb-sliced
