@@ -24,6 +24,8 @@ pytestmark = pytest.mark.skipif(not os.path.exists(CUOBJDUMP), reason="cuobjdump
 C2_MUL = "_ZN3ecm19mulmod_batch_kernelILi6ELi0ELb0ELb1EEEvPKjS2_S2_Pjmjj"
 C2_SQR = "_ZN3ecm19mulmod_batch_kernelILi6ELi0ELb1ELb1EEEvPKjS2_S2_Pjmjj"
 LADDER6 = "_ZN3ecm17ecm_stage1_kernelILi6ELi0ELb0ELb0ELi0EEEvNS_9EcmParamsEPKjjPKmmPjS6_S6_PhS6_j"
+MULMOD = "_ZN3ecm19mulmod_batch_kernelILi{L}ELi0ELb{sq}ELb1EEEvPKjS2_S2_Pjmjj"
+LADDER = "_ZN3ecm17ecm_stage1_kernelILi{L}ELi0ELb0ELb0ELi0EEEvNS_9EcmParamsEPKjjPKmmPjS6_S6_PhS6_j"
 PRODUCT = ("IMAD.WIDE", "IMAD.HI")
 
 
@@ -115,3 +117,18 @@ def test_ladder_step_mix_and_uniform_branches(lib):
         if target == a:  # the trailing self-branch after EXIT
             continue
         assert op.startswith("BRA.U") or t.startswith("BRA"), (hex(a), t)
+
+
+@pytest.mark.parametrize("L", (4, 6, 8, 12, 16))
+def test_every_width_products_per_step_and_spills(lib, L):
+    """Every width's default chains and ladder: 2L^2 / (3L^2+L)/2 products per multiply / square, 6
+    multiplies + 4 squares = 18L^2 + 2L per ladder step, no local memory in the mulmod loops; the ladder
+    loops spill only at L = 12 (held to 168 registers for 3 CTAs/SM): a few words per step."""
+    for sq, per in ((0, 2 * L * L), (1, (3 * L * L + L) // 2)):
+        m = mix(hot_loop(sass(lib, MULMOD.format(L=L, sq=sq)), 2 * per))
+        assert m["products"] % per == 0 and m["imad"] == L * (m["products"] // per), (sq, m)
+        assert m["local"] == 0, (sq, m)
+    m = mix(hot_loop(sass(lib, LADDER.format(L=L)), 18 * L * L))
+    step = 18 * L * L + 2 * L
+    assert step <= m["products"] <= step + 2 and m["imad"] == 10 * L, m
+    assert m["local"] <= (8 if L == 12 else 0), m
